@@ -1,0 +1,227 @@
+"""oracle — plain CPU oracle for the Neural Bounding hot path (ctypes binding).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py, never by the product package
+(paper_2310_06822_b200).  It shares no code with the CUDA path; see
+oracle/nb_oracle.h for the per-function citations into PAPER.md.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnb_oracle.so")
+SRC = os.path.join(HERE, "nb_oracle.c")
+
+POINT, RAY, PLANE, BOX = 0, 1, 2, 3
+KIND = {"point": POINT, "ray": RAY, "plane": PLANE, "box": BOX}
+FP64, BF16_EMU = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(LIB_PATH) or \
+            os.path.getmtime(LIB_PATH) < os.path.getmtime(SRC) or \
+            os.path.getmtime(LIB_PATH) < os.path.getmtime(os.path.join(HERE, "nb_oracle.h")):
+        cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-std=c11",
+               "-shared", "-fPIC", "-o", LIB_PATH, SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+class Arch(C.Structure):
+    _fields_ = [("d0", C.c_int32), ("width", C.c_int32), ("layers", C.c_int32),
+                ("n_heads", C.c_int32), ("head_after", C.c_int32 * 2)]
+
+
+class Counts(C.Structure):
+    _fields_ = [("tp", C.c_uint64), ("fp", C.c_uint64), ("fn", C.c_uint64), ("tn", C.c_uint64),
+                ("exit_hist", C.c_uint64 * 4), ("nonfinite", C.c_uint64)]
+
+    def as_dict(self):
+        return dict(tp=self.tp, fp=self.fp, fn=self.fn, tn=self.tn,
+                    exit_hist=list(self.exit_hist), nonfinite=self.nonfinite)
+
+
+class Stats(C.Structure):
+    _fields_ = [("loss", C.c_double), ("tp", C.c_uint64), ("fp", C.c_uint64),
+                ("fn", C.c_uint64), ("tn", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+        sig = {
+            "ora_indicator": (C.c_int, [P, I32, I32, I32, P]),
+            "ora_label": (C.c_int, [P, I32, I32, I32, I32, P, I64, P]),
+            "ora_label_brute": (C.c_int, [P, I32, I32, I32, I32, P, I64, P]),
+            "ora_sat_build": (None, [P, I32, P]),
+            "ora_encode_bf16": (None, [P, I64, I32, P]),
+            "ora_bf16_rne": (C.c_uint16, [C.c_float]),
+            "ora_num_params": (I64, [P]),
+            "ora_forward": (None, [P, P, P, I64, I32, P]),
+            "ora_loss_grad": (D, [P, P, P, P, I64, I64, D, D, P, P]),
+            "ora_weighted_bce": (D, [D, I32, D, D]),
+            "ora_adam": (None, [I64, P, P, P, I64, D, D, D, D, P]),
+            "ora_alpha": (D, [I64, I64]),
+            "ora_calibrate": (C.c_int, [I32, P, P, I64, P]),
+            "ora_score": (None, [I32, P, P, I64, P, P]),
+            "ora_num_threads": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(_lib, name)
+            f.restype = res
+            f.argtypes = args
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _np(x, dtype):
+    if isinstance(x, torch.Tensor):
+        x = x.detach().cpu().numpy()
+    return np.ascontiguousarray(x, dtype=dtype)
+
+
+def arch_of(cfg) -> Arch:
+    a = Arch()
+    a.d0, a.width, a.layers, a.n_heads = cfg.record_floats, cfg.width, cfg.hidden_layers, cfg.n_heads
+    for k, l in enumerate(cfg.head_after):
+        a.head_after[k] = l
+    return a
+
+
+def make_arch(d0, width, layers, head_after=()) -> Arch:
+    a = Arch()
+    a.d0, a.width, a.layers, a.n_heads = d0, width, layers, len(head_after)
+    for k, l in enumerate(head_after):
+        a.head_after[k] = l
+    return a
+
+
+def num_params(a: Arch) -> int:
+    return int(lib().ora_num_params(C.byref(a)))
+
+
+def label(grid, space_dim, kind, q, brute=False, frames=1) -> np.ndarray:
+    g = _np(grid, np.uint8)
+    q = _np(q, np.float32)
+    R = g.shape[-1]
+    n = q.shape[0]
+    y = np.zeros(n, np.uint8)
+    f = lib().ora_label_brute if brute else lib().ora_label
+    rc = f(_ptr(g), space_dim, R, frames, KIND[kind] if isinstance(kind, str) else kind,
+           _ptr(q), n, _ptr(y))
+    assert rc == 0
+    return y
+
+
+def indicator(grid, space_dim, x, frames=1) -> int:
+    g = _np(grid, np.uint8)
+    xx = np.ascontiguousarray(x, np.float64)
+    return int(lib().ora_indicator(_ptr(g), space_dim, g.shape[-1], frames, _ptr(xx)))
+
+
+def sat(grid) -> np.ndarray:
+    g = _np(grid, np.uint8)
+    R = g.shape[0]
+    S = np.zeros((R + 1,) * 3, np.int32)
+    lib().ora_sat_build(_ptr(g), R, _ptr(S))
+    return S
+
+
+def encode_bf16(q) -> np.ndarray:
+    q = _np(q, np.float32)
+    n, d0 = q.shape
+    out = np.zeros((n, 16), np.uint16)
+    lib().ora_encode_bf16(_ptr(q), n, d0, _ptr(out))
+    return out
+
+
+def forward(a: Arch, theta, q, mode=FP64) -> np.ndarray:
+    th = _np(theta, np.float64)
+    q = _np(q, np.float32)
+    n = q.shape[0]
+    out = np.zeros((n, 1 + a.n_heads), np.float64)
+    lib().ora_forward(C.byref(a), _ptr(th), _ptr(q), n, mode, _ptr(out))
+    return out
+
+
+def loss_grad(a: Arch, theta, q, y, alpha, beta, n_global=None):
+    th = _np(theta, np.float64)
+    q = _np(q, np.float32)
+    yy = _np(y, np.uint8)
+    n = q.shape[0]
+    g = np.zeros(num_params(a), np.float64)
+    st = Stats()
+    loss = lib().ora_loss_grad(C.byref(a), _ptr(th), _ptr(q), _ptr(yy), n,
+                               n if n_global is None else n_global, alpha, beta, _ptr(g),
+                               C.byref(st))
+    return loss, g, dict(loss=st.loss, tp=st.tp, fp=st.fp, fn=st.fn, tn=st.tn)
+
+
+def weighted_bce(z, y, alpha, beta) -> float:
+    return float(lib().ora_weighted_bce(z, y, alpha, beta))
+
+
+def adam(theta, m, v, t, g, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+    """In-place Adam on float64 numpy arrays."""
+    lib().ora_adam(theta.size, _ptr(theta), _ptr(m), _ptr(v), t, lr, b1, b2, eps,
+                   _ptr(_np(g, np.float64)))
+
+
+def alpha(t, T) -> float:
+    return float(lib().ora_alpha(t, T))
+
+
+def calibrate(logits, y):
+    z = _np(logits, np.float64)
+    if z.ndim == 1:
+        z = z[:, None]
+    yy = _np(y, np.uint8)
+    tau = np.zeros(z.shape[1], np.float64)
+    rc = lib().ora_calibrate(z.shape[1] - 1, _ptr(z), _ptr(yy), z.shape[0], _ptr(tau))
+    return tau, rc
+
+
+def score(logits, y, tau) -> dict:
+    z = _np(logits, np.float64)
+    if z.ndim == 1:
+        z = z[:, None]
+    yy = _np(y, np.uint8)
+    t = _np(tau, np.float64)
+    c = Counts()
+    lib().ora_score(z.shape[1] - 1, _ptr(z), _ptr(yy), z.shape[0], _ptr(t), C.byref(c))
+    return c.as_dict()
+
+
+def num_threads() -> int:
+    return int(lib().ora_num_threads())
+
+
+def train(cfg, theta0, batches, T=None, lr=1e-3):
+    """Plain training loop (Alg. 1 + Adam): batches yields (q, y) per step."""
+    a = arch_of(cfg)
+    th = _np(theta0, np.float64).copy()
+    m = np.zeros_like(th)
+    v = np.zeros_like(th)
+    hist = []
+    for t, (q, y) in enumerate(batches):
+        al = alpha(t, T)
+        loss, g, st = loss_grad(a, th, q, y, al, 1.0)
+        adam(th, m, v, t + 1, g, lr=lr)
+        hist.append(st)
+    return th, hist
