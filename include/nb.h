@@ -1,0 +1,198 @@
+/* nb.h — C ABI of the B200-native Neural Bounding hot path (libnb.so).
+ *
+ * The library implements the data-parallel hot path of "Neural Bounding"
+ * (Liu, Fischer, Yoo, Ritschel; arXiv 2310.06822; /root/reference/PAPER.md,
+ * cited as P:<line>):  a small MLP h_theta that classifies encoded
+ * point / ray / plane / box queries as "maybe object" (1) or "certainly not
+ * object" (0) with strictly zero false negatives on its labelled set
+ * (problem statement P:133-145 §3.1, "the FN rate ... must be zero" P:75,
+ * "FP is the only figure of merit" P:372), trained with the asymmetric loss
+ * of Eq. (1) and Alg. 1.
+ *
+ * Conventions for every call (DESIGN.md §4 restates them):
+ *  - Pointers named q, y, x_out, logits, prob, tau_dev are DEVICE pointers on
+ *    the model's device, owned by the caller; the library never frees them.
+ *    Calls whose name ends in _host take HOST pointers instead.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Query records are fp32, row-major [n][nb_record_floats(kind, dim)]:
+ *      point: x (n floats; 4D is (x, y, z, t));  ray: (origin, unit direction);
+ *      plane: (p0, unit normal);  box: (min corner, max corner).
+ *  - Labels y are uint8 in {0, 1}, one per record.
+ *  - The model owns its weights (fp32 master + packed bf16 copy), Adam state,
+ *    thresholds, scratch and communicator; nothing is allocated on the hot path.
+ *  - Calls filling host structs (nb_counts, tau_out, nb_step_stats) synchronise
+ *    `stream`; nb_encode / nb_forward / nb_label are asynchronous.
+ *  - Errors: argument/shape validation happens before any launch (NB_E_ARG,
+ *    NB_E_SHAPE) and leaves outputs untouched.  In-kernel sticky flags report
+ *    non-finite logits (NB_E_NONFINITE) and labels outside {0,1} (NB_E_LABEL)
+ *    on the next synchronising call, whose outputs are still written.
+ *    NB_E_NO_POSITIVES is warning-class: tau = +inf is written.
+ *    CUDA/NCCL failures return NB_E_CUDA / NB_E_NCCL; nb_last_error() gives
+ *    the thread-local detail string.
+ *  - With a communicator (nb_comm_init), n is the LOCAL shard; counts and tau
+ *    returned are GLOBAL (one NCCL allreduce each); nb_train_step allreduces
+ *    the gradient.  All ranks must issue collective calls in the same order.
+ *  - Threading: one writer per model (train_step, calibrate, set_*);
+ *    concurrent nb_forward / nb_score on distinct streams are allowed when the
+ *    model has no communicator.
+ */
+#ifndef NB_H
+#define NB_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NB_OK = 0,
+  NB_E_ARG = 1,          /* null pointer / bad enum / negative size          */
+  NB_E_SHAPE = 2,        /* dimension mismatch (record width, param count)    */
+  NB_E_NONFINITE = 3,    /* some record produced a non-finite logit           */
+  NB_E_LABEL = 4,        /* some label was not 0 or 1                         */
+  NB_E_NO_POSITIVES = 5, /* calibration set without positives: tau = +inf     */
+  NB_E_CUDA = 6,
+  NB_E_NCCL = 7,
+  NB_E_UNSUPPORTED = 8,  /* architecture outside the compiled kernel set      */
+  NB_E_OOM = 9
+} nb_status;
+
+/* Query parameterisations, Suppl. §3.2. */
+typedef enum { NB_POINT = 0, NB_RAY = 1, NB_PLANE = 2, NB_BOX = 3 } nb_query_kind;
+
+/* Arithmetic of the forward/backward contractions.
+ * NB_FP32: fp32 FMA chains on CUDA cores (BASELINE.json configs[0]).
+ * NB_BF16: bf16 weights/activations, fp32 accumulation on tcgen05 tensor cores
+ *          (configs[1..4]); inputs enter as a bf16 (hi, lo) pair (R20). */
+typedef enum { NB_FP32 = 0, NB_BF16 = 1 } nb_precision;
+
+/* MLP architecture (§3.4; Suppl. Tab. 4): d0 -> width x hidden_layers -> 1,
+ * ReLU hidden activations (R1), optional early-exit heads reading hidden
+ * layers head_after[k] (1-based; §3.3, R22). */
+typedef struct {
+  int32_t kind;          /* nb_query_kind                                    */
+  int32_t space_dim;     /* 2, 3 or 4 (4 = 3D + time, points only)          */
+  int32_t width;         /* hidden width w                                   */
+  int32_t hidden_layers; /* L >= 1                                           */
+  int32_t n_heads;       /* 0..2 early-exit heads                            */
+  int32_t head_after[2]; /* 1-based hidden layer read by each head           */
+  int32_t precision;     /* nb_precision                                     */
+} nb_desc;
+
+/* Confusion counts of the calibrated predictor (P:157-176 cost cases);
+ * exit_hist: [0] left at head 1, [1] left at head 2, [2] final negative,
+ * [3] final positive.  tp + fp + fn + tn = n (global under a communicator). */
+typedef struct {
+  uint64_t tp, fp, fn, tn;
+  uint64_t exit_hist[4];
+  uint64_t nonfinite;
+} nb_counts;
+
+/* Batch statistics of one training step: loss value of Eq. (1) (plus head
+ * terms) and the batch confusion counts at the rounding rule z >= 0
+ * — the paper's convergence curves.                    */
+typedef struct {
+  double loss;
+  uint64_t tp, fp, fn, tn;
+} nb_step_stats;
+
+typedef struct nb_model nb_model; /* opaque */
+typedef struct nb_grid nb_grid;   /* opaque: occupancy grid for the GPU labeller */
+
+/* ---- sizes ---------------------------------------------------------------- */
+/* Floats per query record: n for points, 2n for ray/plane/box; -1 if invalid. */
+int64_t nb_record_floats(int32_t kind, int32_t space_dim);
+/* Parameters of the canonical fp32 blob: sum over layers of (d_in + 1) d_out
+ * plus (w + 1) for the output and each head (the 3->50->50->1 net has the
+ * paper's 2,801).  Layout: per hidden layer W_l[out][in] row-major then
+ * b_l; then w_out[w], b_out; then per head u_k[w], c_k.  -1 if invalid.      */
+int64_t nb_num_params(const nb_desc* desc);
+
+const char* nb_status_string(nb_status s);
+/* Detail of the last error on the calling thread ("" if none). */
+const char* nb_last_error(void);
+/* Compute capability major*10+minor of `device`, and whether this build has
+ * kernels for it (sm_100a only).  Returns NB_E_UNSUPPORTED otherwise.      */
+nb_status nb_device_check(int32_t device, int32_t* cc_out);
+
+/* ---- model lifecycle ------------------------------------------------------ */
+/* Allocates all device state on `device`.  Parameters start at zero. */
+nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out);
+void      nb_model_destroy(nb_model* m);
+/* Host fp32 canonical blob of nb_num_params values; resets Adam state/step. */
+nb_status nb_model_set_params(nb_model* m, const float* host, int64_t n);
+nb_status nb_model_get_params(const nb_model* m, float* host, int64_t n);
+/* Thresholds tau[0] (output), tau[1+k] (head k), logit space (R21). */
+nb_status nb_model_set_thresholds(nb_model* m, const float* tau_host, int32_t n);
+nb_status nb_model_get_thresholds(const nb_model* m, float* tau_host, int32_t n);
+/* Gradient dL/dtheta of the last nb_train_step (after the allreduce), fp32 [P],
+ * canonical layout: the parity hook for rows a7/a8 (DESIGN.md §5 P3).       */
+nb_status nb_model_get_grad(const nb_model* m, float* host, int64_t n);
+/* Adam state (checkpoint/resume): m, v as fp32 [P] host arrays, step count. */
+nb_status nb_model_get_adam(const nb_model* m, float* m_host, float* v_host, int64_t* step);
+nb_status nb_model_set_adam(nb_model* m, const float* m_host, const float* v_host, int64_t step);
+
+/* ---- communicator (NCCL over NVLink/NVSwitch) ----------------------------- */
+/* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
+nb_status nb_comm_unique_id(uint8_t id[128]);
+nb_status nb_comm_init(nb_model* m, const uint8_t id[128], int32_t rank, int32_t world);
+/* Query the NCCL library actually loaded: version code (e.g. 22809). */
+nb_status nb_comm_version(int32_t* version);
+
+/* ---- hot path ------------------------------------------------------------- */
+/* a1 encoder (R20).  NB_BF16: x_out is uint16 [n][16] bf16 bit
+ * patterns (hi(0..d0-1), lo(0..d0-1), zeros); NB_FP32: x_out is fp32 [n][d0]
+ * (identity).  The compute calls below encode in-kernel; this exposes the exact
+ * layer-1 operand for parity.                                                 */
+nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream);
+
+/* a1-a4: logits[n][1 + n_heads] (output logit z, then head logits e_k), fp32;
+ * prob (may be NULL): sigmoid(z) [n].                                */
+nb_status nb_forward(const nb_model* m, const float* q, int64_t n, float* logits, float* prob,
+                     void* stream);
+
+/* a6: tau = min over labelled positives of the logit (and of each head logit),
+ * stored in the model and copied to tau_out (host, 1 + n_heads floats).  With
+ * these thresholds the predictor has FN = 0 on this set (BASELINE.json north
+ * star; replaces the fixed eps = 1e-5 of P:772).  No positives: +inf, and
+ * NB_E_NO_POSITIVES.  Under a communicator tau is the global minimum.       */
+nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n, float* tau_out,
+                       void* stream);
+
+/* a1-a5: fused forward + classify + count with the model's thresholds:
+ * yhat = [e_1 >= tau_1] and [e_2 >= tau_2] and [z >= tau]; counts to *out (host). */
+nb_status nb_score(const nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                   nb_counts* out, void* stream);
+/* Same as nb_score with HOST q/y (pinned or pageable): the library streams the
+ * records to the device in chunks, overlapping copies with the fused kernel
+ * (end-to-end serving path).                                              */
+nb_status nb_score_host(const nb_model* m, const float* q_host, const uint8_t* y_host,
+                        int64_t n, nb_counts* out, void* stream);
+
+/* a1-a9: one Adam step on the loss of Eq. (1) over the local batch, normalised
+ * by n_global (R4); alpha, beta are the FN / FP weights of the
+ * current step (a10 schedule, nb_alpha); Adam (0.9, 0.999, 1e-8) with
+ * learning rate lr.  stats may be NULL (no synchronisation).        */
+nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
+                        int64_t n_global, float alpha, float beta, float lr, nb_step_stats* stats,
+                        void* stream);
+
+/* a10: FN weight of step t of T: alpha_t = 1 + 999 t / (T - 1) (R6);
+ * beta_t = 1.                                                               */
+double nb_alpha(int64_t t, int64_t T);
+
+/* ---- ground-truth labeller (harness support, not a hot-path row) ----------- */
+/* Occupancy grid uint8 host array, row-major, axis 0 slowest; 4D grids are
+ * [frames][R][R][R].  Builds a summed-area table on the device for boxes.   */
+nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uint8_t* host,
+                         int32_t device, nb_grid** out);
+void      nb_grid_destroy(nb_grid* g);
+/* y[i] = g(record i) exactly: point lookup, fp64 DDA for rays, SAT for boxes
+ * (R15-R17; g = any f over the region).                    */
+nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NB_H */

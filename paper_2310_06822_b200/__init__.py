@@ -1,0 +1,340 @@
+"""paper_2310_06822_b200 — B200-native Neural Bounding hot path (Python binding).
+
+Thin ctypes marshalling over libnb.so (include/nb.h).  Every step of the path
+runs in the library's CUDA kernels; PyTorch only provides device memory,
+streams and process groups.  There is no CPU fallback: if libnb.so is missing
+or the device is not sm_100, calls raise.
+
+    import paper_2310_06822_b200 as nb
+    m = nb.Model(nb.Desc(kind="point", space_dim=3, width=64, hidden_layers=4,
+                         precision="bf16"), device=0)
+    m.set_params(theta)                      # canonical fp32 blob (CPU tensor)
+    tau = m.calibrate(q, y)                  # q fp32 [n][d0], y uint8 [n] on cuda
+    counts = m.score(q, y)                   # FP/FN/TP/TN of the calibrated predictor
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnb.so")
+
+POINT, RAY, PLANE, BOX = 0, 1, 2, 3
+KINDS = {"point": POINT, "ray": RAY, "plane": PLANE, "box": BOX}
+FP32, BF16 = 0, 1
+PRECISIONS = {"fp32": FP32, "bf16": BF16}
+STATUS = ["NB_OK", "NB_E_ARG", "NB_E_SHAPE", "NB_E_NONFINITE", "NB_E_LABEL",
+          "NB_E_NO_POSITIVES", "NB_E_CUDA", "NB_E_NCCL", "NB_E_UNSUPPORTED", "NB_E_OOM"]
+NB_OK, NB_E_NO_POSITIVES = 0, 5
+
+
+class NBError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{where}: {name}: {detail}")
+
+
+class _Desc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("space_dim", C.c_int32), ("width", C.c_int32),
+                ("hidden_layers", C.c_int32), ("n_heads", C.c_int32),
+                ("head_after", C.c_int32 * 2), ("precision", C.c_int32)]
+
+
+class _Counts(C.Structure):
+    _fields_ = [("tp", C.c_uint64), ("fp", C.c_uint64), ("fn", C.c_uint64), ("tn", C.c_uint64),
+                ("exit_hist", C.c_uint64 * 4), ("nonfinite", C.c_uint64)]
+
+    def as_dict(self):
+        return dict(tp=self.tp, fp=self.fp, fn=self.fn, tn=self.tn,
+                    exit_hist=list(self.exit_hist), nonfinite=self.nonfinite)
+
+
+class _Stats(C.Structure):
+    _fields_ = [("loss", C.c_double), ("tp", C.c_uint64), ("fp", C.c_uint64),
+                ("fn", C.c_uint64), ("tn", C.c_uint64)]
+
+
+# name -> (restype, argtypes); must cover every function declared in include/nb.h
+_P, _I32, _I64, _F, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double
+SIGNATURES = {
+    "nb_record_floats": (_I64, [_I32, _I32]),
+    "nb_num_params": (_I64, [_P]),
+    "nb_status_string": (C.c_char_p, [C.c_int]),
+    "nb_last_error": (C.c_char_p, []),
+    "nb_device_check": (C.c_int, [_I32, _P]),
+    "nb_model_create": (C.c_int, [_P, _I32, _P]),
+    "nb_model_destroy": (None, [_P]),
+    "nb_model_set_params": (C.c_int, [_P, _P, _I64]),
+    "nb_model_get_params": (C.c_int, [_P, _P, _I64]),
+    "nb_model_set_thresholds": (C.c_int, [_P, _P, _I32]),
+    "nb_model_get_thresholds": (C.c_int, [_P, _P, _I32]),
+    "nb_model_get_grad": (C.c_int, [_P, _P, _I64]),
+    "nb_model_get_adam": (C.c_int, [_P, _P, _P, _P]),
+    "nb_model_set_adam": (C.c_int, [_P, _P, _P, _I64]),
+    "nb_comm_unique_id": (C.c_int, [_P]),
+    "nb_comm_init": (C.c_int, [_P, _P, _I32, _I32]),
+    "nb_comm_version": (C.c_int, [_P]),
+    "nb_encode": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "nb_forward": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
+    "nb_calibrate": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_score": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_score_host": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
+    "nb_alpha": (_D, [_I64, _I64]),
+    "nb_grid_create": (C.c_int, [_I32, _I32, _I32, _P, _I32, _P]),
+    "nb_grid_destroy": (None, [_P]),
+    "nb_label": (C.c_int, [_P, _I32, _P, _I64, _P, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libnb.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run python -m paper_2310_06822_b200.build")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, where: str, ok=(NB_OK,)):
+    if status not in ok:
+        raise NBError(status, where, lib().nb_last_error().decode())
+    return status
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _dev_ptr(t: torch.Tensor, dtype, device, name):
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name} must be a CUDA tensor on cuda:{device}")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor")
+    return t.data_ptr()
+
+
+@dataclass(frozen=True)
+class Desc:
+    kind: str = "point"
+    space_dim: int = 3
+    width: int = 64
+    hidden_layers: int = 4
+    head_after: tuple = ()
+    precision: str = "bf16"
+
+    def to_c(self) -> _Desc:
+        d = _Desc()
+        d.kind = KINDS[self.kind]
+        d.space_dim = self.space_dim
+        d.width = self.width
+        d.hidden_layers = self.hidden_layers
+        d.n_heads = len(self.head_after)
+        for k, l in enumerate(self.head_after):
+            d.head_after[k] = l
+        d.precision = PRECISIONS[self.precision]
+        return d
+
+    @property
+    def record_floats(self) -> int:
+        return int(lib().nb_record_floats(KINDS[self.kind], self.space_dim))
+
+    @property
+    def n_heads(self) -> int:
+        return len(self.head_after)
+
+    @property
+    def num_params(self) -> int:
+        d = self.to_c()
+        return int(lib().nb_num_params(C.byref(d)))
+
+
+def alpha(t: int, T: int) -> float:
+    """FN weight of step t of T (row a10; R6). beta = 1."""
+    return float(lib().nb_alpha(t, T))
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().nb_comm_unique_id(buf), "nb_comm_unique_id")
+    return bytes(buf)
+
+
+def comm_version() -> int:
+    v = C.c_int32()
+    _check(lib().nb_comm_version(C.byref(v)), "nb_comm_version")
+    return v.value
+
+
+class Model:
+    """A bounding MLP resident on one GPU (owning weights, Adam state, tau)."""
+
+    def __init__(self, desc: Desc, device: int = 0):
+        self.desc = desc
+        self.device = device
+        self._d = desc.to_c()
+        h = C.c_void_p()
+        _check(lib().nb_model_create(C.byref(self._d), device, C.byref(h)), "nb_model_create")
+        self._h = h
+        self.P = desc.num_params
+        self.d0 = desc.record_floats
+        self.nl = 1 + desc.n_heads
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nb_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state ---------------------------------------------------------
+    def set_params(self, theta: torch.Tensor):
+        t = theta.detach().to("cpu", torch.float32).contiguous()
+        _check(lib().nb_model_set_params(self._h, t.data_ptr(), t.numel()), "nb_model_set_params")
+
+    def get_params(self) -> torch.Tensor:
+        t = torch.empty(self.P, dtype=torch.float32)
+        _check(lib().nb_model_get_params(self._h, t.data_ptr(), self.P), "nb_model_get_params")
+        return t
+
+    def get_grad(self) -> torch.Tensor:
+        t = torch.empty(self.P, dtype=torch.float32)
+        _check(lib().nb_model_get_grad(self._h, t.data_ptr(), self.P), "nb_model_get_grad")
+        return t
+
+    def set_thresholds(self, tau):
+        t = torch.as_tensor(tau, dtype=torch.float32).contiguous()
+        _check(lib().nb_model_set_thresholds(self._h, t.data_ptr(), t.numel()), "set_thresholds")
+
+    def get_thresholds(self) -> torch.Tensor:
+        t = torch.empty(self.nl, dtype=torch.float32)
+        _check(lib().nb_model_get_thresholds(self._h, t.data_ptr(), self.nl), "get_thresholds")
+        return t
+
+    def get_adam(self):
+        m = torch.empty(self.P, dtype=torch.float32)
+        v = torch.empty(self.P, dtype=torch.float32)
+        step = C.c_int64()
+        _check(lib().nb_model_get_adam(self._h, m.data_ptr(), v.data_ptr(), C.byref(step)), "get_adam")
+        return m, v, step.value
+
+    def set_adam(self, m, v, step):
+        m = m.to("cpu", torch.float32).contiguous()
+        v = v.to("cpu", torch.float32).contiguous()
+        _check(lib().nb_model_set_adam(self._h, m.data_ptr(), v.data_ptr(), step), "set_adam")
+
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().nb_comm_init(self._h, buf, rank, world), "nb_comm_init")
+
+    # ---- hot path ------------------------------------------------------
+    def _q(self, q):
+        if q.dim() != 2 or q.shape[1] != self.d0:
+            raise ValueError(f"q must be [n][{self.d0}]")
+        return _dev_ptr(q, torch.float32, self.device, "q")
+
+    def encode(self, q: torch.Tensor) -> torch.Tensor:
+        n = q.shape[0]
+        if self.desc.precision == "bf16":
+            out = torch.empty(n, 16, dtype=torch.int16, device=q.device)
+        else:
+            out = torch.empty(n, self.d0, dtype=torch.float32, device=q.device)
+        _check(lib().nb_encode(self._h, self._q(q), n, out.data_ptr(), _stream(self.device)), "nb_encode")
+        return out
+
+    def forward(self, q: torch.Tensor, prob: bool = False):
+        n = q.shape[0]
+        logits = torch.empty(n, self.nl, dtype=torch.float32, device=q.device)
+        p = torch.empty(n, dtype=torch.float32, device=q.device) if prob else None
+        _check(lib().nb_forward(self._h, self._q(q), n, logits.data_ptr(),
+                                p.data_ptr() if p is not None else None, _stream(self.device)),
+               "nb_forward")
+        return (logits, p) if prob else logits
+
+    def calibrate(self, q: torch.Tensor, y: torch.Tensor, allow_no_positives=False) -> torch.Tensor:
+        n = q.shape[0]
+        tau = torch.empty(self.nl, dtype=torch.float32)
+        ok = (NB_OK, NB_E_NO_POSITIVES) if allow_no_positives else (NB_OK,)
+        _check(lib().nb_calibrate(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
+                                  n, tau.data_ptr(), _stream(self.device)), "nb_calibrate", ok)
+        return tau
+
+    def score(self, q: torch.Tensor, y: torch.Tensor) -> dict:
+        c = _Counts()
+        _check(lib().nb_score(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
+                              q.shape[0], C.byref(c), _stream(self.device)), "nb_score")
+        return c.as_dict()
+
+    def score_host(self, q: torch.Tensor, y: torch.Tensor) -> dict:
+        if q.device.type != "cpu" or y.device.type != "cpu":
+            raise ValueError("score_host takes host tensors")
+        q = q.contiguous()
+        y = y.contiguous()
+        if q.dtype != torch.float32 or y.dtype != torch.uint8 or q.shape[1] != self.d0:
+            raise ValueError("q fp32 [n][d0], y uint8 [n]")
+        c = _Counts()
+        _check(lib().nb_score_host(self._h, q.data_ptr(), y.data_ptr(), q.shape[0], C.byref(c),
+                                   _stream(self.device)), "nb_score_host")
+        return c.as_dict()
+
+    def train_step(self, q, y, alpha: float, beta: float = 1.0, lr: float = 1e-3,
+                   n_global: int | None = None, stats: bool = False):
+        n = q.shape[0]
+        st = _Stats() if stats else None
+        _check(lib().nb_train_step(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
+                                   n, n if n_global is None else n_global, alpha, beta, lr,
+                                   C.byref(st) if st is not None else None, _stream(self.device)),
+               "nb_train_step")
+        if st is not None:
+            return dict(loss=st.loss, tp=st.tp, fp=st.fp, fn=st.fn, tn=st.tn)
+        return None
+
+
+class Grid:
+    """Occupancy grid resident on the GPU for the ground-truth labeller."""
+
+    def __init__(self, occ: torch.Tensor, space_dim: int, device: int = 0):
+        g = occ.detach().to("cpu", torch.uint8).contiguous()
+        frames = g.shape[0] if space_dim == 4 else 1
+        R = g.shape[-1]
+        h = C.c_void_p()
+        _check(lib().nb_grid_create(space_dim, R, frames, g.data_ptr(), device, C.byref(h)),
+               "nb_grid_create")
+        self._h = h
+        self.device = device
+        self.space_dim = space_dim
+
+    def label(self, kind: str, q: torch.Tensor) -> torch.Tensor:
+        n = q.shape[0]
+        y = torch.empty(n, dtype=torch.uint8, device=q.device)
+        _check(lib().nb_label(self._h, KINDS[kind], _dev_ptr(q, torch.float32, self.device, "q"),
+                              n, y.data_ptr(), _stream(self.device)), "nb_label")
+        return y
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nb_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

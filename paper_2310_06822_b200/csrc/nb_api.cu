@@ -1,0 +1,610 @@
+// nb_api.cu — the C ABI of include/nb.h: validation, model state, dispatch of
+// the hot-path kernels, sticky-flag reporting and the collectives.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "nb_internal.cuh"
+
+namespace nb {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+static nb_status cuda_fail(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return NB_E_CUDA;
+}
+
+#define NB_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e__ = (call);                           \
+    if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+  } while (0)
+
+static bool desc_valid(const nb_desc* d, int* d0_out) {
+  if (!d) return false;
+  if (d->kind < NB_POINT || d->kind > NB_BOX) return false;
+  if (d->space_dim < 2 || d->space_dim > 4) return false;
+  if (d->space_dim == 4 && d->kind != NB_POINT) return false;
+  if (d->width < 1 || d->width > 256) return false;
+  if (d->hidden_layers < 1 || d->hidden_layers > kMaxLayers) return false;
+  if (d->n_heads < 0 || d->n_heads > 2) return false;
+  for (int k = 0; k < d->n_heads; ++k)
+    if (d->head_after[k] < 1 || d->head_after[k] > d->hidden_layers) return false;
+  if (d->n_heads == 2 && d->head_after[0] >= d->head_after[1]) return false;
+  if (d->precision != NB_FP32 && d->precision != NB_BF16) return false;
+  int d0 = d->kind == NB_POINT ? d->space_dim : 2 * d->space_dim;
+  if (d0 > 8) return false;
+  if (d0_out) *d0_out = d0;
+  return true;
+}
+
+static void param_offsets(const nb_desc& d, int d0, ParamOffsets* o) {
+  int64_t p = 0, in = d0;
+  for (int l = 0; l < d.hidden_layers; ++l) {
+    o->W[l] = p; p += in * d.width;
+    o->b[l] = p; p += d.width;
+    in = d.width;
+  }
+  o->wout = p; p += d.width;
+  o->bout = p; p += 1;
+  for (int k = 0; k < 2; ++k) {
+    if (k < d.n_heads) {
+      o->u[k] = p; p += d.width;
+      o->c[k] = p; p += 1;
+    } else {
+      o->u[k] = o->c[k] = 0;
+    }
+  }
+}
+
+static uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+static void pack_layout(const nb_desc& d, PackLayout* pl) {
+  uint32_t off = 0;
+  const uint32_t W = (uint32_t)d.width;
+  for (int l = 0; l < d.hidden_layers; ++l) {
+    const uint32_t K = l == 0 ? (uint32_t)kEncK : W;
+    pl->off_w[l] = off;
+    pl->k_of[l] = K;
+    off = align_up(off + W * K * 2u, 128u);
+  }
+  pl->off_bias = off; off = align_up(off + 4u * W * d.hidden_layers, 16u);
+  pl->off_wout = off; off = align_up(off + 4u * W, 16u);
+  pl->off_bout = off; off += 16u;
+  for (int k = 0; k < 2; ++k) {
+    pl->off_u[k] = off;
+    if (k < d.n_heads) off = align_up(off + 4u * W, 16u);
+  }
+  pl->off_c = off; off += 16u;
+  pl->bytes = align_up(off, 16u);
+}
+
+// Report sticky in-kernel flags (and clear them).  Host mirror is pinned.
+static nb_status take_flags(nb_model* m, cudaStream_t s, nb_status ok) {
+  unsigned int f = 0;
+  NB_CUDA(cudaMemcpyAsync(&f, m->d_flags, sizeof(f), cudaMemcpyDeviceToHost, s));
+  NB_CUDA(cudaStreamSynchronize(s));
+  if (f) NB_CUDA(cudaMemsetAsync(m->d_flags, 0, sizeof(unsigned int), s));
+  if (f & kFlagLabel) {
+    set_error("label outside {0,1}");
+    return NB_E_LABEL;
+  }
+  if (f & kFlagNonFinite) {
+    set_error("non-finite logit");
+    return NB_E_NONFINITE;
+  }
+  return ok;
+}
+
+static cudaError_t launch_forward_any(const nb_model* m, int mode, const FwdArgs& a,
+                                      cudaStream_t s) {
+  if (m->d.precision == NB_BF16) return launch_fwd_tc(m, mode, a, s);
+  return launch_fwd_simt(m, mode, a, s);
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace nb
+
+using namespace nb;
+
+extern "C" {
+
+int64_t nb_record_floats(int32_t kind, int32_t space_dim) {
+  if (kind < NB_POINT || kind > NB_BOX || space_dim < 2 || space_dim > 4) return -1;
+  if (space_dim == 4 && kind != NB_POINT) return -1;
+  return kind == NB_POINT ? space_dim : 2 * space_dim;
+}
+
+int64_t nb_num_params(const nb_desc* d) {
+  int d0;
+  if (!desc_valid(d, &d0)) return -1;
+  int64_t n = 0, in = d0;
+  for (int l = 0; l < d->hidden_layers; ++l) {
+    n += (in + 1) * (int64_t)d->width;
+    in = d->width;
+  }
+  return n + (int64_t)(d->width + 1) * (1 + d->n_heads);
+}
+
+const char* nb_status_string(nb_status s) {
+  switch (s) {
+    case NB_OK: return "ok";
+    case NB_E_ARG: return "invalid argument";
+    case NB_E_SHAPE: return "shape mismatch";
+    case NB_E_NONFINITE: return "non-finite value";
+    case NB_E_LABEL: return "label outside {0,1}";
+    case NB_E_NO_POSITIVES: return "no positive labels (tau = +inf)";
+    case NB_E_CUDA: return "CUDA error";
+    case NB_E_NCCL: return "NCCL error";
+    case NB_E_UNSUPPORTED: return "unsupported configuration";
+    case NB_E_OOM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+const char* nb_last_error(void) { return g_err.c_str(); }
+
+nb_status nb_device_check(int32_t device, int32_t* cc_out) {
+  int major = 0, minor = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (cc_out) *cc_out = major * 10 + minor;
+  if (major != 10 || minor != 0) {
+    set_error("libnb is built for sm_100a only (device cc %d.%d)", major, minor);
+    return NB_E_UNSUPPORTED;
+  }
+  return NB_OK;
+}
+
+nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
+  int d0;
+  if (!out || !desc_valid(desc, &d0)) {
+    set_error("invalid nb_desc");
+    return NB_E_ARG;
+  }
+  const bool ok_arch = desc->precision == NB_BF16 ? tc_supported(*desc) : simt_supported(*desc);
+  if (!ok_arch) {
+    set_error("no kernel for precision %d width %d", desc->precision, desc->width);
+    return NB_E_UNSUPPORTED;
+  }
+  nb_status st = nb_device_check(device, nullptr);
+  if (st != NB_OK) return st;
+  DeviceGuard g(device);
+  nb_model* m = new nb_model();
+  m->d = *desc;
+  for (int k = desc->n_heads; k < 2; ++k) m->d.head_after[k] = 0;
+  m->device = device;
+  m->d0 = d0;
+  m->P = nb_num_params(desc);
+  param_offsets(m->d, d0, &m->po);
+  pack_layout(m->d, &m->pl);
+  cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes);
+  };
+  A((void**)&m->theta, sizeof(float) * m->P);
+  A((void**)&m->adam_m, sizeof(float) * m->P);
+  A((void**)&m->adam_v, sizeof(float) * m->P);
+  A((void**)&m->grad, sizeof(float) * m->P);
+  A((void**)&m->packed, m->pl.bytes);
+  A((void**)&m->d_tau, sizeof(float) * 4);
+  A((void**)&m->d_counts, sizeof(unsigned long long) * 16);
+  A((void**)&m->d_keys, sizeof(unsigned int) * 4);
+  A((void**)&m->d_flags, sizeof(unsigned int) * 4);
+  A((void**)&m->d_loss, sizeof(double) * 2);
+  A((void**)&m->d_stats, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&m->h_pinned, 256);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&m->ev_copy[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_done[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    nb_model_destroy(m);
+    set_error("nb_model_create: %s", cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? NB_E_OOM : NB_E_CUDA;
+  }
+  if (m->d.precision == NB_BF16) {
+    e = launch_pack_bf16(m, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      nb_model_destroy(m);
+      return cuda_fail(e, "pack");
+    }
+  }
+  *out = m;
+  return NB_OK;
+}
+
+void nb_model_destroy(nb_model* m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  comm_destroy(m);
+  cudaFree(m->theta);
+  cudaFree(m->adam_m);
+  cudaFree(m->adam_v);
+  cudaFree(m->grad);
+  cudaFree(m->packed);
+  cudaFree(m->d_tau);
+  cudaFree(m->d_counts);
+  cudaFree(m->d_keys);
+  cudaFree(m->d_flags);
+  cudaFree(m->d_loss);
+  cudaFree(m->d_stats);
+  cudaFree(m->train_scratch);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(m->stage_q[i]);
+    cudaFree(m->stage_y[i]);
+    if (m->ev_copy[i]) cudaEventDestroy(m->ev_copy[i]);
+    if (m->ev_done[i]) cudaEventDestroy(m->ev_done[i]);
+  }
+  if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->h_pinned) cudaFreeHost(m->h_pinned);
+  delete m;
+}
+
+nb_status nb_model_set_params(nb_model* m, const float* host, int64_t n) {
+  if (!m || !host) return set_error("null argument"), NB_E_ARG;
+  if (n != m->P) return set_error("expected %lld params, got %lld", (long long)m->P, (long long)n), NB_E_SHAPE;
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(host[i])) return set_error("non-finite parameter %lld", (long long)i), NB_E_NONFINITE;
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaMemcpy(m->theta, host, sizeof(float) * n, cudaMemcpyHostToDevice));
+  NB_CUDA(cudaMemset(m->adam_m, 0, sizeof(float) * n));
+  NB_CUDA(cudaMemset(m->adam_v, 0, sizeof(float) * n));
+  m->step = 0;
+  if (m->d.precision == NB_BF16) {
+    NB_CUDA(launch_pack_bf16(m, 0));
+    NB_CUDA(cudaDeviceSynchronize());
+  }
+  return NB_OK;
+}
+
+nb_status nb_model_get_params(const nb_model* m, float* host, int64_t n) {
+  if (!m || !host) return set_error("null argument"), NB_E_ARG;
+  if (n != m->P) return set_error("expected %lld params", (long long)m->P), NB_E_SHAPE;
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaDeviceSynchronize());
+  NB_CUDA(cudaMemcpy(host, m->theta, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  return NB_OK;
+}
+
+nb_status nb_model_get_grad(const nb_model* m, float* host, int64_t n) {
+  if (!m || !host) return set_error("null argument"), NB_E_ARG;
+  if (n != m->P) return set_error("expected %lld params", (long long)m->P), NB_E_SHAPE;
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaDeviceSynchronize());
+  NB_CUDA(cudaMemcpy(host, m->grad, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  return NB_OK;
+}
+
+nb_status nb_model_get_adam(const nb_model* m, float* mh, float* vh, int64_t* step) {
+  if (!m || !mh || !vh || !step) return set_error("null argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaDeviceSynchronize());
+  NB_CUDA(cudaMemcpy(mh, m->adam_m, sizeof(float) * m->P, cudaMemcpyDeviceToHost));
+  NB_CUDA(cudaMemcpy(vh, m->adam_v, sizeof(float) * m->P, cudaMemcpyDeviceToHost));
+  *step = m->step;
+  return NB_OK;
+}
+
+nb_status nb_model_set_adam(nb_model* m, const float* mh, const float* vh, int64_t step) {
+  if (!m || !mh || !vh || step < 0) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaMemcpy(m->adam_m, mh, sizeof(float) * m->P, cudaMemcpyHostToDevice));
+  NB_CUDA(cudaMemcpy(m->adam_v, vh, sizeof(float) * m->P, cudaMemcpyHostToDevice));
+  m->step = step;
+  return NB_OK;
+}
+
+nb_status nb_model_set_thresholds(nb_model* m, const float* tau, int32_t n) {
+  if (!m || !tau) return set_error("null argument"), NB_E_ARG;
+  if (n != 1 + m->d.n_heads) return set_error("expected %d thresholds", 1 + m->d.n_heads), NB_E_SHAPE;
+  for (int k = 0; k < n; ++k) m->tau[k] = tau[k];
+  DeviceGuard g(m->device);
+  NB_CUDA(cudaMemcpy(m->d_tau, m->tau, sizeof(float) * 3, cudaMemcpyHostToDevice));
+  return NB_OK;
+}
+
+nb_status nb_model_get_thresholds(const nb_model* m, float* tau, int32_t n) {
+  if (!m || !tau) return set_error("null argument"), NB_E_ARG;
+  if (n != 1 + m->d.n_heads) return set_error("expected %d thresholds", 1 + m->d.n_heads), NB_E_SHAPE;
+  for (int k = 0; k < n; ++k) tau[k] = m->tau[k];
+  return NB_OK;
+}
+
+nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream) {
+  if (!m || n < 0 || (n > 0 && (!q || !x_out))) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  NB_CUDA(launch_encode(m, q, n, x_out, (cudaStream_t)stream));
+  return NB_OK;
+}
+
+static FwdArgs base_args(const nb_model* m, const float* q, const uint8_t* y, int64_t n) {
+  FwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.q = q;
+  a.y = y;
+  a.n = n;
+  for (int k = 0; k < 3; ++k) a.tau[k] = m->tau[k];
+  a.counts = m->d_counts;
+  a.keys = m->d_keys;
+  a.flags = m->d_flags;
+  return a;
+}
+
+nb_status nb_forward(const nb_model* m, const float* q, int64_t n, float* logits, float* prob,
+                     void* stream) {
+  if (!m || n < 0 || (n > 0 && (!q || !logits))) return set_error("bad argument"), NB_E_ARG;
+  if (n == 0) return NB_OK;
+  DeviceGuard g(m->device);
+  FwdArgs a = base_args(m, q, nullptr, n);
+  a.logits = logits;
+  a.prob = prob;
+  NB_CUDA(launch_forward_any(m, kForward, a, (cudaStream_t)stream));
+  return NB_OK;
+}
+
+nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n, float* tau_out,
+                       void* stream) {
+  if (!m || !tau_out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nl = 1 + m->d.n_heads;
+  NB_CUDA(cudaMemsetAsync(m->d_keys, 0xFF, sizeof(unsigned int) * 4, s));
+  if (n > 0) NB_CUDA(launch_forward_any(m, kCalibrate, base_args(m, q, y, n), s));
+  if (m->comm && comm_allreduce_u32_min(m, m->d_keys, nl, s))
+    return NB_E_NCCL;
+  unsigned int* hk = (unsigned int*)m->h_pinned;
+  NB_CUDA(cudaMemcpyAsync(hk, m->d_keys, sizeof(unsigned int) * 4, cudaMemcpyDeviceToHost, s));
+  NB_CUDA(cudaStreamSynchronize(s));
+  bool none = false;
+  for (int k = 0; k < nl; ++k) {
+    if (hk[k] == 0xFFFFFFFFu) {
+      m->tau[k] = INFINITY;
+      none = true;
+    } else {
+      m->tau[k] = key2f(hk[k]);
+    }
+    tau_out[k] = m->tau[k];
+  }
+  NB_CUDA(cudaMemcpyAsync(m->d_tau, m->tau, sizeof(float) * 3, cudaMemcpyHostToDevice, s));
+  nb_status st = take_flags(m, s, NB_OK);
+  if (st != NB_OK) return st;
+  if (none) {
+    set_error("calibration set has no positives");
+    return NB_E_NO_POSITIVES;
+  }
+  return NB_OK;
+}
+
+static void counts_out(const unsigned long long* c, nb_counts* out) {
+  out->tp = c[0]; out->fp = c[1]; out->fn = c[2]; out->tn = c[3];
+  for (int k = 0; k < 4; ++k) out->exit_hist[k] = c[4 + k];
+  out->nonfinite = c[8];
+}
+
+nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t n, nb_counts* out,
+                   void* stream) {
+  nb_model* m = const_cast<nb_model*>(m_);
+  if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
+  if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
+  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
+  unsigned long long* hc = m->h_pinned;
+  NB_CUDA(cudaMemcpyAsync(hc, m->d_counts, sizeof(unsigned long long) * kNumCounters,
+                          cudaMemcpyDeviceToHost, s));
+  NB_CUDA(cudaStreamSynchronize(s));
+  counts_out(hc, out);
+  return take_flags(m, s, NB_OK);
+}
+
+nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, int64_t n,
+                        nb_counts* out, void* stream) {
+  nb_model* m = const_cast<nb_model*>(m_);
+  if (!m || !out || n < 0 || (n > 0 && (!qh || !yh))) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t chunk = (int64_t)1 << 20;  // rows per staged chunk (multiple of 128)
+  if (m->stage_rows < chunk) {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(m->stage_q[i]);
+      cudaFree(m->stage_y[i]);
+      m->stage_q[i] = nullptr;
+      m->stage_y[i] = nullptr;
+      NB_CUDA(cudaMalloc((void**)&m->stage_q[i], sizeof(float) * chunk * m->d0));
+      NB_CUDA(cudaMalloc((void**)&m->stage_y[i], chunk));
+    }
+    m->stage_rows = chunk;
+  }
+  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
+  // the copy stream may only start once the counters are reset / prior work done
+  NB_CUDA(cudaEventRecord(m->ev_done[0], s));
+  NB_CUDA(cudaEventRecord(m->ev_done[1], s));
+  int64_t i = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += chunk, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t rows = std::min(chunk, n - r0);
+    NB_CUDA(cudaStreamWaitEvent(m->copy_stream, m->ev_done[b], 0));
+    NB_CUDA(cudaMemcpyAsync(m->stage_q[b], qh + r0 * m->d0, sizeof(float) * rows * m->d0,
+                            cudaMemcpyHostToDevice, m->copy_stream));
+    NB_CUDA(cudaMemcpyAsync(m->stage_y[b], yh + r0, rows, cudaMemcpyHostToDevice, m->copy_stream));
+    NB_CUDA(cudaEventRecord(m->ev_copy[b], m->copy_stream));
+    NB_CUDA(cudaStreamWaitEvent(s, m->ev_copy[b], 0));
+    NB_CUDA(launch_forward_any(m, kScore, base_args(m, m->stage_q[b], m->stage_y[b], rows), s));
+    NB_CUDA(cudaEventRecord(m->ev_done[b], s));
+  }
+  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
+  unsigned long long* hc = m->h_pinned;
+  NB_CUDA(cudaMemcpyAsync(hc, m->d_counts, sizeof(unsigned long long) * kNumCounters,
+                          cudaMemcpyDeviceToHost, s));
+  NB_CUDA(cudaStreamSynchronize(s));
+  counts_out(hc, out);
+  return take_flags(m, s, NB_OK);
+}
+
+nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
+                        int64_t n_global, float alpha, float beta, float lr, nb_step_stats* stats,
+                        void* stream) {
+  if (!m || n_local < 0 || n_global < n_local || n_global <= 0 ||
+      (n_local > 0 && (!q || !y)))
+    return set_error("bad argument"), NB_E_ARG;
+  if (!(alpha > 0.f) || !(beta >= 0.f) || !(lr > 0.f)) return set_error("bad alpha/beta/lr"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = m->d.precision == NB_BF16;
+  if (tc && !train_tc_supported(m->d)) {
+    set_error("bf16 training not built for width %d", m->d.width);
+    return NB_E_UNSUPPORTED;
+  }
+  if (!tc && m->d.width > 32) {
+    set_error("fp32 training supports width <= 32");
+    return NB_E_UNSUPPORTED;
+  }
+  size_t need = tc ? train_tc_scratch_bytes(m, n_local) : train_simt_scratch_bytes(m, n_local);
+  if (need > m->train_scratch_bytes) {
+    NB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(m->train_scratch);
+    m->train_scratch = nullptr;
+    m->train_scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&m->train_scratch, need);
+    if (e != cudaSuccess) return set_error("train scratch: %s", cudaGetErrorString(e)), NB_E_OOM;
+    m->train_scratch_bytes = need;
+  }
+  NB_CUDA(cudaMemsetAsync(m->d_loss, 0, sizeof(double), s));
+  NB_CUDA(cudaMemsetAsync(m->d_stats, 0, sizeof(unsigned long long) * 4, s));
+  if (tc)
+    NB_CUDA(launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s));
+  else
+    NB_CUDA(launch_train_simt(m, q, y, n_local, n_global, alpha, beta, s));
+  if (m->comm) {
+    if (comm_allreduce_f32_sum(m, m->grad, m->P, s)) return NB_E_NCCL;
+  }
+  NB_CUDA(launch_adam(m, lr, s));
+  if (tc) NB_CUDA(launch_pack_bf16(m, s));
+  if (stats) {
+    if (m->comm) {
+      if (comm_allreduce_f64_sum(m, m->d_loss, 1, s)) return NB_E_NCCL;
+      if (comm_allreduce_u64_sum(m, m->d_stats, 4, s)) return NB_E_NCCL;
+    }
+    unsigned long long* hs = m->h_pinned;
+    NB_CUDA(cudaMemcpyAsync(hs, m->d_stats, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+    NB_CUDA(cudaMemcpyAsync(hs + 4, m->d_loss, sizeof(double), cudaMemcpyDeviceToHost, s));
+    NB_CUDA(cudaStreamSynchronize(s));
+    stats->tp = hs[0]; stats->fp = hs[1]; stats->fn = hs[2]; stats->tn = hs[3];
+    double l;
+    memcpy(&l, hs + 4, sizeof(double));
+    stats->loss = l;
+    return take_flags(m, s, NB_OK);
+  }
+  return NB_OK;
+}
+
+double nb_alpha(int64_t t, int64_t T) {
+  if (T <= 1) return 1000.0;
+  return 1.0 + 999.0 * (double)t / (double)(T - 1);
+}
+
+nb_status nb_comm_unique_id(uint8_t id[128]) {
+  if (!id) return set_error("null id"), NB_E_ARG;
+  return comm_unique_id(id) ? NB_E_NCCL : NB_OK;
+}
+
+nb_status nb_comm_init(nb_model* m, const uint8_t id[128], int32_t rank, int32_t world) {
+  if (!m || !id || world < 1 || rank < 0 || rank >= world) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  return comm_init(m, id, rank, world) ? NB_E_NCCL : NB_OK;
+}
+
+nb_status nb_comm_version(int32_t* v) {
+  if (!v) return NB_E_ARG;
+  int vv = 0;
+  if (comm_version(&vv)) return NB_E_NCCL;
+  *v = vv;
+  return NB_OK;
+}
+
+nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uint8_t* host,
+                         int32_t device, nb_grid** out) {
+  if (!host || !out || space_dim < 2 || space_dim > 4 || R < 1 || R > 4096 ||
+      (space_dim == 4 && frames < 1))
+    return set_error("bad grid"), NB_E_ARG;
+  DeviceGuard g(device);
+  nb_grid* gr = new nb_grid();
+  gr->space_dim = space_dim;
+  gr->R = R;
+  gr->frames = space_dim == 4 ? frames : 1;
+  gr->device = device;
+  size_t cells = (size_t)gr->frames;
+  for (int j = 0; j < (space_dim == 4 ? 3 : space_dim); ++j) cells *= (size_t)R;
+  cudaError_t e = cudaMalloc((void**)&gr->occ, cells);
+  if (e == cudaSuccess) e = cudaMemcpy(gr->occ, host, cells, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && space_dim == 3) {
+    e = cudaMalloc((void**)&gr->sat, sizeof(int32_t) * (size_t)(R + 1) * (R + 1) * (R + 1));
+    if (e == cudaSuccess) e = launch_sat_build(gr, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  if (e != cudaSuccess) {
+    nb_grid_destroy(gr);
+    return cuda_fail(e, "nb_grid_create");
+  }
+  *out = gr;
+  return NB_OK;
+}
+
+void nb_grid_destroy(nb_grid* g) {
+  if (!g) return;
+  DeviceGuard dg(g->device);
+  cudaFree(g->occ);
+  cudaFree(g->sat);
+  delete g;
+}
+
+nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
+                   void* stream) {
+  if (!g || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  if (kind == NB_POINT) {
+    // ok for any dim
+  } else if (g->space_dim != 3 || (kind != NB_RAY && kind != NB_BOX)) {
+    set_error("GPU labeller supports points (2D/3D/4D), 3D rays and 3D boxes");
+    return NB_E_UNSUPPORTED;
+  }
+  if (n == 0) return NB_OK;
+  DeviceGuard dg(g->device);
+  NB_CUDA(launch_label(g, kind, q, n, y, (cudaStream_t)stream));
+  return NB_OK;
+}
+
+}  // extern "C"

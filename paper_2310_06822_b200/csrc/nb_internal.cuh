@@ -1,0 +1,145 @@
+// nb_internal.cuh — internal declarations of libnb.so (not part of the ABI).
+//
+// Product code only: nothing here is shared with oracle/ (which must stay an
+// independent implementation of the paper).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/nb.h"
+
+namespace nb {
+
+constexpr int kMaxLayers = 8;
+constexpr int kTile = 128;          // rows per MMA tile (M = 128)
+constexpr int kEncK = 16;           // layer-1 K after the bf16 (hi, lo) split
+constexpr int kNumCounters = 9;     // tp fp fn tn exit[4] nonfinite
+constexpr uint32_t kFlagNonFinite = 1u, kFlagLabel = 2u;
+
+void set_error(const char* fmt, ...);
+
+// Byte layout of the packed bf16 parameter image that a CTA copies into shared
+// memory once (cp.async.bulk).  B operands are K-major, no-swizzle UMMA core
+// matrices: element (n, k) of an [N][K] matrix sits at
+//   (n / 8) * SBO + (k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2,  SBO = K / 8 * 128.
+struct PackLayout {
+  uint32_t off_w[kMaxLayers];  // layer l B image (layer 0: [W][16], others [W][W])
+  uint32_t k_of[kMaxLayers];   // K of each layer image (16 or W)
+  uint32_t off_bias;           // fp32 [L][W]
+  uint32_t off_wout;           // fp32 [W]
+  uint32_t off_bout;           // fp32 (padded to 16 B)
+  uint32_t off_u[2];           // fp32 [W] per head
+  uint32_t off_c;              // fp32 [2] head biases (padded)
+  uint32_t bytes;              // total, multiple of 16
+};
+
+struct ParamOffsets {  // canonical fp32 blob offsets (nb.h nb_num_params)
+  int64_t W[kMaxLayers], b[kMaxLayers], wout, bout, u[2], c[2];
+};
+
+}  // namespace nb
+
+struct nb_model {
+  nb_desc d;
+  int device = 0;
+  int d0 = 0;
+  int64_t P = 0;
+  int num_sms = 0;
+  nb::ParamOffsets po;
+  nb::PackLayout pl;
+  float* theta = nullptr;     // fp32 master, canonical layout [P]
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  float* grad = nullptr;      // [P] gradient of the current step
+  int64_t step = 0;
+  uint8_t* packed = nullptr;  // bf16 packed image (pl.bytes)
+  float tau[3] = {0, 0, 0};
+  float* d_tau = nullptr;     // [3]
+  unsigned long long* d_counts = nullptr;  // [kNumCounters]
+  unsigned int* d_keys = nullptr;          // [3] order-preserving min keys
+  unsigned int* d_flags = nullptr;         // sticky flags
+  double* d_loss = nullptr;                // [1]
+  unsigned long long* d_stats = nullptr;   // [4] batch tp fp fn tn
+  unsigned long long* h_pinned = nullptr;  // pinned host mirror for small readbacks
+  // training scratch (grown on demand outside the timed hot path)
+  void* train_scratch = nullptr;
+  size_t train_scratch_bytes = 0;
+  // host-buffer serving path
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  float* stage_q[2] = {nullptr, nullptr};
+  uint8_t* stage_y[2] = {nullptr, nullptr};
+  int64_t stage_rows = 0;
+  // communicator
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+struct nb_grid {
+  int space_dim = 0, R = 0, frames = 1, device = 0;
+  uint8_t* occ = nullptr;   // device copy of the grid
+  int32_t* sat = nullptr;   // (R+1)^3 summed-area table (3D only)
+};
+
+namespace nb {
+
+// ---- launchers (each returns cudaGetLastError of its launch) ---------------
+enum Mode { kForward = 0, kCalibrate = 1, kScore = 2 };
+
+struct FwdArgs {
+  const float* q;
+  const uint8_t* y;
+  int64_t n;
+  float* logits;
+  float* prob;
+  float tau[3];
+  unsigned long long* counts;
+  unsigned int* keys;
+  unsigned int* flags;
+};
+
+cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s);
+cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t s);
+cudaError_t launch_fwd_simt(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
+cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
+bool tc_supported(const nb_desc& d);
+bool simt_supported(const nb_desc& d);
+
+cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                              int64_t n_global, float alpha, float beta, cudaStream_t s);
+cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                            int64_t n_global, float alpha, float beta, cudaStream_t s);
+bool train_tc_supported(const nb_desc& d);
+size_t train_tc_scratch_bytes(const nb_model* m, int64_t n);
+size_t train_simt_scratch_bytes(const nb_model* m, int64_t n);
+cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s);
+cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, uint8_t* y,
+                         cudaStream_t s);
+cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);
+
+// NCCL (dlopen'ed); all return 0 on success
+int comm_unique_id(uint8_t id[128]);
+int comm_init(nb_model* m, const uint8_t id[128], int rank, int world);
+void comm_destroy(nb_model* m);
+int comm_allreduce_u64_sum(nb_model* m, unsigned long long* buf, size_t count, cudaStream_t s);
+int comm_allreduce_u32_min(nb_model* m, unsigned int* buf, size_t count, cudaStream_t s);
+int comm_allreduce_f32_sum(nb_model* m, float* buf, size_t count, cudaStream_t s);
+int comm_allreduce_f64_sum(nb_model* m, double* buf, size_t count, cudaStream_t s);
+int comm_version(int* v);
+
+// order-preserving fp32 <-> u32 key (min of keys == key of min)
+__host__ __device__ inline uint32_t f2key(float f) {
+  uint32_t b;
+  memcpy(&b, &f, 4);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__host__ __device__ inline float key2f(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+}
+
+}  // namespace nb

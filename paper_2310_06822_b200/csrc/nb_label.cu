@@ -1,0 +1,153 @@
+// nb_label.cu — ground-truth labeller on the GPU (harness support, not a
+// hot-path row): y = g(record) = any f over the region,
+// the exact readings of DESIGN.md R15-R17:
+//   point: f(x) = grid[min(R-1, floor(x R))...], 0 outside [0,1]^n;
+//   ray:   positive-length traversal of an occupied half-open voxel cell
+//          (Amanatides-Woo in fp64);
+//   box:   any occupied cell in [cell(lo), cell(hi)] via a summed-area table.
+// This file is compiled with -fmad=false so every fp64 operation is rounded
+// exactly as written (no FMA contraction).
+#include <stdint.h>
+
+#include "nb_internal.cuh"
+
+namespace nb {
+
+__device__ __forceinline__ int cell_of(double x, int R) {
+  long long i = (long long)floor(x * (double)R);
+  return (int)(i > R - 1 ? R - 1 : i);
+}
+
+__device__ int label_point(const nb_grid g, const float* r) {
+  const int sd = g.space_dim;
+  for (int j = 0; j < sd; ++j) {
+    double v = (double)r[j];
+    if (!(v >= 0.0 && v <= 1.0)) return 0;
+  }
+  const int R = g.R;
+  if (sd == 2) return g.occ[(size_t)cell_of(r[0], R) * R + cell_of(r[1], R)] != 0;
+  size_t idx = ((size_t)cell_of(r[0], R) * R + cell_of(r[1], R)) * R + cell_of(r[2], R);
+  if (sd == 4) idx += (size_t)cell_of(r[3], g.frames) * R * R * R;
+  return g.occ[idx] != 0;
+}
+
+__device__ int label_ray(const nb_grid g, const float* r) {
+  const int R = g.R;
+  double o[3] = {r[0], r[1], r[2]}, d[3] = {r[3], r[4], r[5]};
+  // clip the half-line s >= 0 to the closed unit cube (slab test)
+  double s0 = 0.0, s1 = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    if (d[a] == 0.0) {
+      if (o[a] < 0.0 || o[a] > 1.0) return 0;
+    } else {
+      double ta = (0.0 - o[a]) / d[a], tb = (1.0 - o[a]) / d[a];
+      double lo = ta < tb ? ta : tb, hi = ta < tb ? tb : ta;
+      s0 = lo > s0 ? lo : s0;
+      s1 = hi < s1 ? hi : s1;
+    }
+  }
+  if (!(s1 > s0)) return 0;
+  int cell[3], dir[3];
+  double next[3];
+  for (int a = 0; a < 3; ++a) {
+    const double xr = (o[a] + s0 * d[a]) * (double)R;
+    long long c = (long long)floor(xr);
+    if (d[a] < 0.0 && (double)c == xr) c -= 1;  // entering downward through a face
+    c = c < 0 ? 0 : (c > R - 1 ? R - 1 : c);
+    cell[a] = (int)c;
+    dir[a] = d[a] > 0.0 ? 1 : (d[a] < 0.0 ? -1 : 0);
+    if (dir[a] > 0) next[a] = ((double)(cell[a] + 1) / (double)R - o[a]) / d[a];
+    else if (dir[a] < 0) next[a] = ((double)cell[a] / (double)R - o[a]) / d[a];
+    else next[a] = INFINITY;
+  }
+  double s = s0;
+  while (true) {
+    const int a = (next[0] <= next[1]) ? ((next[0] <= next[2]) ? 0 : 2)
+                                       : ((next[1] <= next[2]) ? 1 : 2);
+    const double e = next[a] < s1 ? next[a] : s1;
+    if (e > s && g.occ[((size_t)cell[0] * R + cell[1]) * R + cell[2]]) return 1;
+    if (!(next[a] < s1)) return 0;
+    s = e;
+    cell[a] += dir[a];
+    if (cell[a] < 0 || cell[a] >= R) return 0;
+    next[a] = (dir[a] > 0 ? ((double)(cell[a] + 1) / (double)R - o[a])
+                          : ((double)cell[a] / (double)R - o[a])) / d[a];
+  }
+}
+
+__device__ int label_box(const nb_grid g, const float* r) {
+  const int R = g.R;
+  int a[3], b[3];
+  for (int j = 0; j < 3; ++j) {
+    double lo = r[j], hi = r[3 + j];
+    lo = lo < 0.0 ? 0.0 : lo;
+    hi = hi > 1.0 ? 1.0 : hi;
+    if (!(hi >= lo)) return 0;
+    a[j] = cell_of(lo, R);
+    b[j] = cell_of(hi, R) + 1;
+  }
+  const size_t R1 = (size_t)R + 1;
+  auto S = [&](int i, int j, int k) -> long long { return g.sat[((size_t)i * R1 + j) * R1 + k]; };
+  long long c = S(b[0], b[1], b[2]) - S(a[0], b[1], b[2]) - S(b[0], a[1], b[2]) -
+                S(b[0], b[1], a[2]) + S(a[0], a[1], b[2]) + S(a[0], b[1], a[2]) +
+                S(b[0], a[1], a[2]) - S(a[0], a[1], a[2]);
+  return c > 0;
+}
+
+__global__ void k_label(const nb_grid g, int kind, const float* __restrict__ q, int64_t n,
+                        uint8_t* __restrict__ y) {
+  const int nf = kind == NB_POINT ? g.space_dim : 2 * g.space_dim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float r[8];
+    for (int j = 0; j < nf; ++j) r[j] = q[i * nf + j];
+    int v = 0;
+    if (kind == NB_POINT) v = label_point(g, r);
+    else if (kind == NB_RAY) v = label_ray(g, r);
+    else v = label_box(g, r);
+    y[i] = (uint8_t)v;
+  }
+}
+
+cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, uint8_t* y,
+                         cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  k_label<<<blocks, 256, 0, s>>>(*g, kind, q, n, y);
+  return cudaGetLastError();
+}
+
+// Summed-area table: three prefix-sum passes, one per axis, over (R+1)^3 with a
+// zero border.  S[i][j][k] = number of occupied cells (i' < i, j' < j, k' < k).
+__global__ void k_sat_init(const uint8_t* __restrict__ occ, int R, int32_t* __restrict__ S) {
+  const size_t R1 = (size_t)R + 1, tot = R1 * R1 * R1;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < tot;
+       t += (size_t)gridDim.x * blockDim.x) {
+    int k = (int)(t % R1), j = (int)((t / R1) % R1), i = (int)(t / (R1 * R1));
+    S[t] = (i && j && k) ? occ[((size_t)(i - 1) * R + (j - 1)) * R + (k - 1)] : 0;
+  }
+}
+
+__global__ void k_sat_scan(int R, int axis, int32_t* __restrict__ S) {
+  const size_t R1 = (size_t)R + 1;
+  const size_t lines = R1 * R1;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < lines;
+       t += (size_t)gridDim.x * blockDim.x) {
+    size_t u = t / R1, v = t % R1, base, stride;
+    if (axis == 0) { base = u * R1 + v; stride = R1 * R1; }
+    else if (axis == 1) { base = u * R1 * R1 + v; stride = R1; }
+    else { base = (u * R1 + v) * R1; stride = 1; }
+    int32_t acc = 0;
+    for (size_t i = 0; i < R1; ++i) {
+      acc += S[base + i * stride];
+      S[base + i * stride] = acc;
+    }
+  }
+}
+
+cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s) {
+  k_sat_init<<<1024, 256, 0, s>>>(g->occ, g->R, g->sat);
+  for (int ax = 0; ax < 3; ++ax) k_sat_scan<<<256, 128, 0, s>>>(g->R, ax, g->sat);
+  return cudaGetLastError();
+}
+
+}  // namespace nb

@@ -1,0 +1,58 @@
+"""Shared helpers for the GPU parity tests (test infrastructure only)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import nbgen
+import oracle
+import paper_2310_06822_b200 as nb
+
+BAND = 1e-3  # BASELINE.json: counts bit-exact excluding |logit - tau| < 1e-3 (R28)
+
+
+def desc_of(cfg: nbgen.Config, precision=None) -> nb.Desc:
+    return nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
+                   precision or cfg.precision)
+
+
+_GRIDS = {}
+
+
+def grid_of(cfg):
+    key = cfg.name if cfg.name in nbgen.CONFIGS else repr(cfg.grid)
+    if key not in _GRIDS:
+        _GRIDS[key] = nbgen.make_grid(cfg).numpy()
+    return _GRIDS[key]
+
+
+def labels_oracle(cfg, q: np.ndarray) -> np.ndarray:
+    g = grid_of(cfg)
+    frames = g.shape[0] if cfg.space_dim == 4 else 1
+    return oracle.label(g, cfg.space_dim, cfg.kind, q, frames=frames)
+
+
+def scaled_params(cfg, seed=0, scale=2.5, bias=0.3) -> torch.Tensor:
+    """Xavier init made 'trained-like': larger weights and random biases so
+    logits spread over several units (a harder parity case than init)."""
+    th = nbgen.init_params(cfg).double()
+    rng = np.random.default_rng(seed)
+    th = th * scale + torch.from_numpy(rng.normal(size=th.numel())) * bias / np.sqrt(cfg.width)
+    return th.float()
+
+
+def sigmoid(z):
+    return 1.0 / (1.0 + np.exp(-z))
+
+
+def band_mask(z_a, tau_a, z_b, tau_b):
+    """Rows whose logit (any head) lies within BAND of either side's threshold."""
+    m = np.zeros(z_a.shape[0], bool)
+    for k in range(z_a.shape[1]):
+        m |= np.abs(z_a[:, k] - tau_a[k]) < BAND
+        m |= np.abs(z_b[:, k] - tau_b[k]) < BAND
+    return m
+
+
+def counts_from_logits(z, y, tau):
+    return oracle.score(z, y, tau)

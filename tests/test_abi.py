@@ -1,0 +1,50 @@
+"""CPU checks of the C ABI: libnb.so loads without a GPU and exports every
+function include/nb.h declares; host-only entry points answer correctly."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2310_06822_b200 as nb
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "nb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(nb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_five_hot_path_calls():
+    fns = declared_functions()
+    for f in ["nb_encode", "nb_forward", "nb_train_step", "nb_calibrate", "nb_score"]:
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol():
+    L = C.CDLL(nb.LIB_PATH)
+    missing = [f for f in declared_functions() if not hasattr(L, f)]
+    assert not missing, missing
+    assert set(declared_functions()) == set(nb.SIGNATURES), \
+        set(declared_functions()) ^ set(nb.SIGNATURES)
+
+
+def test_host_only_calls():
+    L = nb.lib()
+    assert L.nb_record_floats(nb.POINT, 3) == 3
+    assert L.nb_record_floats(nb.RAY, 3) == 6
+    assert L.nb_record_floats(nb.POINT, 4) == 4
+    assert L.nb_record_floats(nb.RAY, 4) == -1
+    assert nb.Desc("point", 3, 50, 2, precision="fp32").num_params == 2801
+    assert nb.Desc("point", 4, 128, 6, (2, 4)).num_params == 83587
+    assert nb.alpha(0, 200) == 1.0 and nb.alpha(199, 200) == 1000.0
+    assert L.nb_status_string(5) == b"no positive labels (tau = +inf)"
+
+
+def test_invalid_desc_rejected_without_gpu():
+    d = nb.Desc("ray", 4, 64, 4).to_c()
+    assert nb.lib().nb_num_params(C.byref(d)) == -1
+    h = C.c_void_p()
+    assert nb.lib().nb_model_create(C.byref(d), 0, C.byref(h)) == 1  # NB_E_ARG

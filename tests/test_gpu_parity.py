@@ -1,0 +1,244 @@
+"""GPU parity tests: the CUDA path through the C ABI against the oracle on the
+same seeded inputs (protocol P1-P6; tolerances from
+BASELINE.json north_star).  All marked gpu."""
+import numpy as np
+import pytest
+import torch
+
+import nbgen
+import oracle
+import paper_2310_06822_b200 as nb
+from gpu_helpers import (BAND, band_mask, desc_of, grid_of, labels_oracle, scaled_params,
+                         sigmoid)
+
+pytestmark = pytest.mark.gpu
+DEV = 0
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cc = nb.C.c_int32()
+    assert nb.lib().nb_device_check(DEV, nb.C.byref(cc)) == 0, "libnb needs sm_100"
+
+
+def cuda(t):
+    return torch.as_tensor(t).to(f"cuda:{DEV}").contiguous()
+
+
+# ---------------------------------------------------------------- labeller (P6)
+@pytest.mark.parametrize("name,n", [("c1", 1 << 16), ("c2", 1 << 18), ("c3", 1 << 16),
+                                    ("c4", 1 << 18), ("c5", 1 << 18)])
+def test_labeller_bit_exact(name, n):
+    cfg = nbgen.CONFIGS[name]
+    q = nbgen.make_queries(cfg, nbgen.TAG_HOLDOUT, 0, n)
+    y_ref = labels_oracle(cfg, q.numpy())
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), cfg.space_dim, DEV)
+    y = g.label(cfg.kind, cuda(q)).cpu().numpy()
+    assert np.array_equal(y, y_ref), int((y != y_ref).sum())
+    assert 0 < y.mean() < 1
+
+
+def test_labeller_ray_edge_cases():
+    cfg = nbgen.CONFIGS["c3"]
+    R = 64
+    rng = np.random.default_rng(0)
+    o = np.round(rng.random((20000, 3)) * R) / R
+    d = np.eye(3)[rng.integers(0, 3, 20000)] * rng.choice([-1, 1], (20000, 1))
+    d[10000:] = rng.normal(size=(10000, 3))
+    d[10000:] /= np.linalg.norm(d[10000:], axis=1, keepdims=True)
+    q = np.concatenate([o, d], 1).astype(np.float32)
+    y_ref = oracle.label(grid_of(cfg), 3, "ray", q)
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), 3, DEV)
+    assert np.array_equal(g.label("ray", cuda(q)).cpu().numpy(), y_ref)
+
+
+# ---------------------------------------------------------------- encoder (a1)
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_encode_bit_exact(name):
+    cfg = nbgen.CONFIGS[name]
+    if cfg.width > 128:
+        pytest.skip("w=256 kernel not built yet")
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 5000)
+    m = nb.Model(desc_of(cfg), DEV)
+    x = m.encode(cuda(q)).cpu().numpy().view(np.uint16)
+    assert np.array_equal(x, oracle.encode_bf16(q.numpy()))
+
+
+# ---------------------------------------------------------------- fp32 path (c1)
+def test_c1_fp32_forward_within_1e5():
+    cfg = nbgen.CONFIGS["c1"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, cfg.n_eval)
+    m = nb.Model(desc_of(cfg), DEV)
+    for th in (nbgen.init_params(cfg), scaled_params(cfg, 1)):
+        m.set_params(th)
+        z, p = m.forward(cuda(q), prob=True)
+        z = z.cpu().double().numpy()
+        zr = oracle.forward(oracle.arch_of(cfg), th.double().numpy(), q.numpy())
+        err = np.abs(z - zr) / np.maximum(1.0, np.abs(zr))
+        assert err.max() <= 1e-5, err.max()
+        assert np.allclose(p.cpu().numpy(), sigmoid(zr[:, 0]), atol=1e-6)
+
+
+def test_c1_calibrate_score_counts():
+    cfg = nbgen.CONFIGS["c1"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, cfg.n_eval)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 2)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    qd, yd = cuda(q), cuda(y)
+    tau = m.calibrate(qd, yd).numpy()
+    c = m.score(qd, yd)
+    zr = oracle.forward(oracle.arch_of(cfg), th.double().numpy(), q.numpy())
+    tr, _ = oracle.calibrate(zr, y)
+    cr = oracle.score(zr, y, tr)
+    assert c["fn"] == 0 and cr["fn"] == 0                     # P5
+    assert c["tp"] + c["fn"] == int(y.sum())
+    zg = m.forward(qd).cpu().double().numpy()
+    keep = ~band_mask(zg, tau, zr, tr)
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(zr[keep], y[keep], tr)
+    for k in ("tp", "fp", "fn", "tn"):
+        assert cg[k] == co[k], (k, cg, co)                     # P4
+
+
+def test_c1_train_step_gradient_parity():
+    cfg = nbgen.CONFIGS["c1"]
+    q = nbgen.train_batch(cfg, 0)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 3)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    st = m.train_step(cuda(q), cuda(y), alpha=37.0, beta=1.0, lr=1e-3, stats=True)
+    g = m.get_grad().double().numpy()
+    loss, gr, sr = oracle.loss_grad(oracle.arch_of(cfg), th.double().numpy(), q.numpy(), y, 37.0, 1.0)
+    assert abs(st["loss"] - loss) <= 1e-4 * abs(loss)
+    assert np.linalg.norm(g - gr) <= 1e-4 * np.linalg.norm(gr)
+    assert (st["tp"], st["fn"]) == (sr["tp"], sr["fn"])
+    # Adam step applied to the fp32 master weights
+    th1 = m.get_params().double().numpy()
+    mm, vv = np.zeros_like(gr), np.zeros_like(gr)
+    ref = th.double().numpy().copy()
+    oracle.adam(ref, mm, vv, 1, g)
+    assert np.allclose(th1, ref, atol=2e-6)
+
+
+def test_c1_training_run_conservative():
+    """200 Adam steps (BASELINE.json configs[0]); whole trajectory: parity
+    unpinned (chaotic), checked by invariants: FN = 0 after calibration and
+    FP below the initial network's."""
+    cfg = nbgen.CONFIGS["c1"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, cfg.n_eval)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    m = nb.Model(desc_of(cfg), DEV)
+    th0 = nbgen.init_params(cfg)
+    m.set_params(th0)
+    m.calibrate(qd, yd)
+    fp0 = m.score(qd, yd)["fp"]
+    T = cfg.train_steps
+    for t in range(T):
+        sl = slice((t % 16) * 4096, (t % 16 + 1) * 4096)
+        m.train_step(qd[sl], yd[sl], alpha=nb.alpha(t, T))
+    m.calibrate(qd, yd)
+    c = m.score(qd, yd)
+    assert c["fn"] == 0 and c["fp"] < fp0
+
+
+# ---------------------------------------------------------------- bf16 tensor-core path
+BF16_CASES = [("c2", (1 << 16) + 77), ("c3", (1 << 15) + 5), ("c4", (1 << 15) + 129)]
+
+
+@pytest.mark.parametrize("name,n", BF16_CASES)
+def test_bf16_forward_sigmoid_within_2e2(name, n):
+    cfg = nbgen.CONFIGS[name]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    th = scaled_params(cfg, 4)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    z, p = m.forward(cuda(q), prob=True)
+    z = z.cpu().double().numpy()
+    a = oracle.arch_of(cfg)
+    zr = oracle.forward(a, th.double().numpy(), q.numpy())           # plain fp64 (P2)
+    assert np.abs(sigmoid(z) - sigmoid(zr)).max() <= 2e-2
+    assert np.abs(p.cpu().numpy() - sigmoid(zr[:, 0])).max() <= 2e-2
+    ze = oracle.forward(a, th.double().numpy(), q.numpy(), oracle.BF16_EMU)  # kernel precision
+    close = np.abs(z - ze) < BAND
+    assert close.mean() > 0.99, close.mean()
+
+
+@pytest.mark.parametrize("name,n", BF16_CASES)
+def test_bf16_calibrate_score_counts(name, n):
+    cfg = nbgen.CONFIGS[name]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 5)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    qd, yd = cuda(q), cuda(y)
+    tau = m.calibrate(qd, yd).numpy()
+    c = m.score(qd, yd)
+    assert c["fn"] == 0                                               # P5 GPU
+    assert sum(c[k] for k in ("tp", "fp", "fn", "tn")) == n
+    assert sum(c["exit_hist"]) == n
+    zg = m.forward(qd).cpu().double().numpy()
+    # the fused score kernel and the forward kernel produce identical logits
+    cf = oracle.score(zg, y, tau)
+    for k in ("tp", "fp", "fn", "tn"):
+        assert cf[k] == c[k]
+    assert cf["exit_hist"] == c["exit_hist"]
+    ze = oracle.forward(oracle.arch_of(cfg), th.double().numpy(), q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    ce = oracle.score(ze, y, te)
+    assert ce["fn"] == 0                                              # P5 oracle
+    keep = ~band_mask(zg, tau, ze, te)
+    assert keep.mean() > 0.95
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    for k in ("tp", "fp", "fn", "tn"):
+        assert cg[k] == co[k], (k, cg, co)                            # P4
+
+
+@pytest.mark.parametrize("n", [0, 1, 127, 128, 129, 255, 257, 128 * 148 * 2 + 1])
+def test_bf16_edge_sizes(n):
+    cfg = nbgen.CONFIGS["c2"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, max(n, 1))[:n]
+    th = scaled_params(cfg, 6)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    z = m.forward(cuda(q)).cpu().double().numpy()
+    assert z.shape == (n, 1)
+    if n:
+        zr = oracle.forward(oracle.arch_of(cfg), th.double().numpy(), q.numpy())
+        assert np.abs(sigmoid(z) - sigmoid(zr)).max() <= 2e-2
+    c = m.score(cuda(q), cuda(np.zeros(n, np.uint8)))
+    assert c["tp"] + c["fp"] + c["fn"] + c["tn"] == n
+
+
+def test_score_host_equals_score():
+    cfg = nbgen.CONFIGS["c2"]
+    n = (1 << 21) + 333
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), 3, DEV)
+    qd = cuda(q)
+    yd = g.label("point", qd)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 7))
+    m.calibrate(qd, yd)
+    c1 = m.score(qd, yd)
+    c2 = m.score_host(q, yd.cpu())
+    assert c1 == c2 and c1["fn"] == 0
+
+
+def test_no_positives_and_bad_labels():
+    cfg = nbgen.CONFIGS["c2"]
+    q = cuda(nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 1000))
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 8))
+    tau = m.calibrate(q, cuda(np.zeros(1000, np.uint8)), allow_no_positives=True)
+    assert np.isinf(tau[0].item())
+    with pytest.raises(nb.NBError) as e:
+        m.score(q, cuda(np.full(1000, 2, np.uint8)))
+    assert e.value.status == 4  # NB_E_LABEL
