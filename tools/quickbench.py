@@ -1,5 +1,7 @@
 """Quick device-time measurement of the fused score kernel (dev tool)."""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import time
 
 import torch
