@@ -1,0 +1,355 @@
+"""bench.py — the driver's benchmark contract for the Neural Bounding hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the fused hot path (encode -> MLP on tcgen05 -> classify
+with the calibrated threshold -> FP/FN/TP/TN counts -> NCCL allreduce of the
+counts across ranks) over one batch of BASELINE.json configs[1] ("c2": 3D
+point bounding, 3 -> 64x4 -> 1 bf16, 2^22 uniform points per forward pass).
+Inputs are seeded synthetic (nbgen), labels come from the library's GPU
+labeller, thresholds from nb_calibrate; the timed region is nb_score only.
+
+Weak scaling: every rank scores its own 2^22-query shard (rows r*2^22.. of the
+EVAL stream); value = all ranks' queries / max-over-ranks device time.
+L2 (126 MB) is flushed by writing a 256 MiB buffer between timed steps (the
+step's inputs are 52 MB), outside the timed events.
+
+--impl reference times the oracle (oracle/, plain C fp64) on the host cores on
+a bounded sample of the same workload; under torchrun only rank
+0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "c2"
+N_PER_RANK = 1 << 22
+METRIC = "bounding queries/s"
+UNIT = "queries/s"
+
+
+def flop_per_query(cfg) -> int:
+    """Algorithmic flops of one forward: 2 * MACs of all layers
+    + output head (+ exit heads), unpadded."""
+    macs = cfg.record_floats * cfg.width + (cfg.hidden_layers - 1) * cfg.width ** 2
+    macs += cfg.width * (1 + cfg.n_heads)
+    return 2 * macs
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    """dram bytes per launch of the score kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        k = d.get(CONFIG, {}).get("score_kernel", {})
+        if "dram_bytes_per_launch" in k:
+            return k["dram_bytes_per_launch"], k.get("tensor_pipe_pct")
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    """Oracle (plain C, fp64) on host cores: forward + calibrated score."""
+    import torch
+
+    import nbgen
+    import oracle
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = nbgen.CONFIGS[CONFIG]
+    oracle.build()
+    a = oracle.arch_of(cfg)
+    grid = nbgen.make_grid(cfg).numpy()
+    th = (nbgen.init_params(cfg) * 2.5).double().numpy()
+    n = args.ref_sample
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n).numpy()
+    y = oracle.label(grid, 3, "point", q)
+    z = oracle.forward(a, th, q)  # warm, and the calibration pass
+    tau, _ = oracle.calibrate(z, y)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        oracle.score(oracle.forward(a, th, q[:4096]), y[:4096], tau)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        c = oracle.score(oracle.forward(a, th, q), y, tau)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = n / t
+    cores = oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{CONFIG}: 3D point bounding, 3->64x4->1, oracle sample of {n} "
+                               f"points per step (full step is 2^22)", "global_batch": n},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{n} c2 EVAL points, fp64 forward + calibrated score"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0, "counts_sample": {k: c[k] for k in ("tp", "fp", "fn", "tn")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(n=1 << 18):
+    """The oracle as it stands on this host's cores (bounded sample)."""
+    import nbgen
+    import oracle
+
+    cfg = nbgen.CONFIGS[CONFIG]
+    oracle.build()
+    a = oracle.arch_of(cfg)
+    th = (nbgen.init_params(cfg) * 2.5).double().numpy()
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n).numpy()
+    y = oracle.label(nbgen.make_grid(cfg).numpy(), 3, "point", q)
+    t0 = time.perf_counter()
+    z = oracle.forward(a, th, q)
+    tau, _ = oracle.calibrate(z, y)
+    oracle.score(z, y, tau)
+    t = time.perf_counter() - t0
+    return {"value": n / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} c2 EVAL points: fp64 forward + calibrate + score ({t:.1f} s)"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import nbgen
+    import paper_2310_06822_b200 as nb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = nbgen.CONFIGS[CONFIG]
+    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
+    m = nb.Model(desc, local)
+    if world > 1:
+        uid = [nb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        m.comm_init(uid[0], rank, world)
+    m.set_params(nbgen.init_params(cfg) * 2.5)
+    n = N_PER_RANK
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
+    grid = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
+    y = grid.label(cfg.kind, q)
+    tau = m.calibrate(q, y)                       # global tau (allreduce min across ranks)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return m.score(q, y)
+
+    for _ in range(args.warmup):
+        c = step()
+    assert c["fn"] == 0, c
+    # ---------------- timed region (device time, per-step events) ----------------
+    m.set_timing(True)
+    m.kernel_time()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                 # evict the inputs from L2 (untimed)
+            evs[i][0].record(stream)
+            c = step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kernel_ms, launches = m.kernel_time()
+    m.set_timing(False)
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([dev_ms, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, kernel_ms = t.tolist()
+    total_q = n * world * args.steps
+    value = total_q / (dev_ms * 1e-3)
+    # ---------------- roofline of the dominant kernel ----------------
+    fq = flop_per_query(cfg)
+    peak, peak_src = load_peaks()
+    per_launch_ms = kernel_ms / max(1, launches)
+    achieved = fq * n / (per_launch_ms * 1e-3) / 1e12
+    traffic, tensor_pct = load_traffic()
+    # ---------------- end to end: host buffers through the C ABI ----------------
+    q_h = q.cpu().pin_memory()
+    y_h = y.cpu().pin_memory()
+    for _ in range(2):
+        m.score_host(q_h, y_h)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        ce = m.score_host(q_h, y_h)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = total_q / (e2e_ms.item() * 1e-3)
+    assert ce == c, (ce, c)
+    # ---------------- train samples/s (BASELINE.json metric part 2) ----------------
+    train = None
+    if args.train_steps > 0:
+        train = train_rate(nb, nbgen, cfg, local, rank, world, args.train_steps)
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{CONFIG}: BASELINE.json configs[1], 3D point bounding, "
+                                   "3->64x4->1 ReLU bf16 (fp32 accumulate), 2^22 uniform points per "
+                                   "rank per step, fused forward+calibrated score+counts",
+                       "global_batch": n * world, "per_rank_batch": n,
+                       "parallelism": f"dp{world} (query shards, NCCL allreduce of counts)",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_fwd_tc<64,4,0,0,kScore>", "flop_per_query": fq,
+                         "kernel_ms_per_launch": per_launch_ms,
+                         "ncu_tensor_pipe_pct": tensor_pct},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (4 * cfg.record_floats + 1),
+                    "d2h_bytes_per_step": 9 * 8, "api": "nb_score_host (pinned host q/y)"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "counts": {k: c[k] for k in ("tp", "fp", "fn", "tn")},
+            "tau": float(tau[0]),
+        }
+        if train is not None:
+            line["train"] = train
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def train_rate(nb, nbgen, cfg, local, rank, world, steps):
+    """Training samples/s of the fp32 configs[0] path (bf16 training: see DESIGN.md)."""
+    import torch
+
+    c1 = nbgen.CONFIGS["c1"]
+    desc = nb.Desc(c1.kind, c1.space_dim, c1.width, c1.hidden_layers, (), c1.precision)
+    m = nb.Model(desc, local)
+    m.set_params(nbgen.init_params(c1))
+    g = nb.Grid(nbgen.make_grid(c1), 2, local)
+    q = nbgen.make_queries(c1, nbgen.TAG_EVAL, 0, c1.n_eval, device=f"cuda:{local}")
+    y = g.label("point", q)
+    B = c1.train_batch
+    for t in range(3):
+        m.train_step(q[:B], y[:B], alpha=1.0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(steps):
+        sl = slice((t % 16) * B, (t % 16 + 1) * B)
+        m.train_step(q[sl], y[sl], alpha=nb.alpha(t, steps))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"metric": "train samples/s", "value": B * steps / (ms * 1e-3), "config": "c1 fp32 2->32x2->1, batch 4096",
+            "steps": steps, "ms_per_step": ms / steps}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 23)
+    ap.add_argument("--train-steps", type=int, default=50)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,13 @@ nb_status nb_model_get_grad(const nb_model* m, float* host, int64_t n);
 nb_status nb_model_get_adam(const nb_model* m, float* m_host, float* v_host, int64_t* step);
 nb_status nb_model_set_adam(nb_model* m, const float* m_host, const float* v_host, int64_t step);
 
+/* Kernel-time instrumentation: when enabled, CUDA events bracket every
+ * hot-path kernel launch of this model on the caller's stream (adding one
+ * event synchronisation per launch).  nb_model_kernel_time returns the summed
+ * device time (ms) and launch count since the previous call, then resets.  */
+nb_status nb_model_set_timing(nb_model* m, int32_t enable);
+nb_status nb_model_kernel_time(nb_model* m, double* ms, int64_t* launches);
+
 /* ---- communicator (NCCL over NVLink/NVSwitch) ----------------------------- */
 /* 128-byte NCCL unique id, produced on rank 0 and broadcast by the caller. */
 nb_status nb_comm_unique_id(uint8_t id[128]);

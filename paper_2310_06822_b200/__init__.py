@@ -76,6 +76,8 @@ SIGNATURES = {
     "nb_model_get_grad": (C.c_int, [_P, _P, _I64]),
     "nb_model_get_adam": (C.c_int, [_P, _P, _P, _P]),
     "nb_model_set_adam": (C.c_int, [_P, _P, _P, _I64]),
+    "nb_model_set_timing": (C.c_int, [_P, _I32]),
+    "nb_model_kernel_time": (C.c_int, [_P, _P, _P]),
     "nb_comm_unique_id": (C.c_int, [_P]),
     "nb_comm_init": (C.c_int, [_P, _P, _I32, _I32]),
     "nb_comm_version": (C.c_int, [_P]),
@@ -239,6 +241,16 @@ class Model:
         m = m.to("cpu", torch.float32).contiguous()
         v = v.to("cpu", torch.float32).contiguous()
         _check(lib().nb_model_set_adam(self._h, m.data_ptr(), v.data_ptr(), step), "set_adam")
+
+    def set_timing(self, enable: bool):
+        _check(lib().nb_model_set_timing(self._h, 1 if enable else 0), "nb_model_set_timing")
+
+    def kernel_time(self):
+        """(device ms, launches) of the bracketed hot-path kernels since last call."""
+        ms = C.c_double()
+        k = C.c_int64()
+        _check(lib().nb_model_kernel_time(self._h, C.byref(ms), C.byref(k)), "nb_model_kernel_time")
+        return ms.value, k.value
 
     def comm_init(self, uid: bytes, rank: int, world: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

@@ -111,10 +111,28 @@ static nb_status take_flags(nb_model* m, cudaStream_t s, nb_status ok) {
   return ok;
 }
 
+// Kernel-time instrumentation (nb_model_set_timing): CUDA events bracket the
+// hot-path kernel launches on the caller's stream; the elapsed time of all
+// bracketed launches since the last nb_model_kernel_ms() call is accumulated.
+static bool timing_on(const nb_model* m) { return m->timing && m->ev_used < nb_model::kEvPool; }
+static void timing_begin(const nb_model* m, cudaStream_t s) {
+  if (timing_on(m)) cudaEventRecord(m->ev_pool[2 * m->ev_used], s);
+}
+static void timing_end(const nb_model* m, cudaStream_t s) {
+  if (!timing_on(m)) return;
+  nb_model* mm = const_cast<nb_model*>(m);
+  cudaEventRecord(mm->ev_pool[2 * mm->ev_used + 1], s);
+  mm->ev_used += 1;
+  mm->kernel_launches += 1;
+}
+
 static cudaError_t launch_forward_any(const nb_model* m, int mode, const FwdArgs& a,
                                       cudaStream_t s) {
-  if (m->d.precision == NB_BF16) return launch_fwd_tc(m, mode, a, s);
-  return launch_fwd_simt(m, mode, a, s);
+  timing_begin(m, s);
+  cudaError_t e = m->d.precision == NB_BF16 ? launch_fwd_tc(m, mode, a, s)
+                                            : launch_fwd_simt(m, mode, a, s);
+  timing_end(m, s);
+  return e;
 }
 
 struct DeviceGuard {
@@ -269,6 +287,10 @@ void nb_model_destroy(nb_model* m) {
     if (m->ev_done[i]) cudaEventDestroy(m->ev_done[i]);
   }
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->ev_pool) {
+    for (int i = 0; i < 2 * nb_model::kEvPool; ++i) cudaEventDestroy(m->ev_pool[i]);
+    delete[] m->ev_pool;
+  }
   if (m->h_pinned) cudaFreeHost(m->h_pinned);
   delete m;
 }
@@ -305,6 +327,36 @@ nb_status nb_model_get_grad(const nb_model* m, float* host, int64_t n) {
   DeviceGuard g(m->device);
   NB_CUDA(cudaDeviceSynchronize());
   NB_CUDA(cudaMemcpy(host, m->grad, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  return NB_OK;
+}
+
+nb_status nb_model_set_timing(nb_model* m, int32_t enable) {
+  if (!m) return set_error("null model"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  if (enable && !m->ev_pool) {
+    m->ev_pool = new cudaEvent_t[2 * nb_model::kEvPool];
+    for (int i = 0; i < 2 * nb_model::kEvPool; ++i) NB_CUDA(cudaEventCreate(&m->ev_pool[i]));
+  }
+  m->timing = enable ? 1 : 0;
+  m->ev_used = 0;
+  m->kernel_launches = 0;
+  return NB_OK;
+}
+
+nb_status nb_model_kernel_time(nb_model* m, double* ms, int64_t* launches) {
+  if (!m || !ms || !launches) return set_error("null argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  double tot = 0.0;
+  for (int i = 0; i < m->ev_used; ++i) {
+    NB_CUDA(cudaEventSynchronize(m->ev_pool[2 * i + 1]));
+    float t = 0.f;
+    NB_CUDA(cudaEventElapsedTime(&t, m->ev_pool[2 * i], m->ev_pool[2 * i + 1]));
+    tot += t;
+  }
+  *ms = tot;
+  *launches = m->ev_used;
+  m->ev_used = 0;
+  m->kernel_launches = 0;
   return NB_OK;
 }
 

@@ -75,6 +75,12 @@ struct nb_model {
   // communicator
   void* comm = nullptr;
   int rank = 0, world = 1;
+  // kernel-time instrumentation (off by default)
+  int timing = 0;
+  static constexpr int kEvPool = 4096;     // event pairs recorded without host syncs
+  cudaEvent_t* ev_pool = nullptr;          // [2 * kEvPool]
+  int ev_used = 0;
+  int64_t kernel_launches = 0;
 };
 
 struct nb_grid {
