@@ -35,7 +35,26 @@ struct TcParams {
   PackLayout pl;
   int d0, L, nh, ha0, ha1;
   int64_t num_tiles;
+  unsigned long long* trace;  // NB_TRACE builds only: timeline of CTA 0
 };
+
+#ifdef NB_TRACE
+// Debug timeline (tools/trace_fwd.py): each tracing thread of CTA 0 owns a
+// region of 2000 (clock64, code) pairs; stores only, no atomics on the path.
+#define NB_TR(region, code)                                                          \
+  do {                                                                               \
+    if (blockIdx.x == 0 && p.trace && tr_i < 2000) {                                 \
+      p.trace[((region) * 2000 + tr_i) * 2] = clock64();                            \
+      p.trace[((region) * 2000 + tr_i) * 2 + 1] = (unsigned long long)(code);       \
+      ++tr_i;                                                                        \
+    }                                                                                \
+  } while (0)
+#else
+#define NB_TR(region, code) \
+  do {                      \
+  } while (0)
+#endif
+#define NB_EV(type, s, l) ((type) | ((s) << 4) | ((l) << 8))
 
 __device__ __forceinline__ void encode_cols(const float* x, int d0, uint32_t (&col)[8]) {
   uint32_t h[8], l[8];
@@ -137,31 +156,39 @@ struct TcPlan;
 template <>
 struct TcPlan<32> { static constexpr int NSLOT = 4, WPS = 4, COLS = 256; };
 template <>
-struct TcPlan<64> { static constexpr int NSLOT = 4, WPS = 4, COLS = 512; };
+struct TcPlan<64> { static constexpr int NSLOT = 5, WPS = 4, COLS = 512; };
 template <>
 struct TcPlan<128> { static constexpr int NSLOT = 2, WPS = 8, COLS = 512; };
 
 // LC / H0C / H1C: compile-time layer count and exit-head layers (1-based, 0 =
 // none) of the specialised instantiations; LC == 0 selects the generic kernel
 // that reads them from TcParams at run time.
+//
+// There is no dedicated MMA warp: each slot's lead warp (lane quarter 0,
+// column half 0) issues its own slot's MMAs right after the slot's warps
+// meet at a named barrier, so every slot is an independent chain
+//   [stage A in TMEM] -> bar.sync -> MMA layer l -> commit -> acc_full ->
+//   [epilogue l: ld, bias, ReLU, bf16 pack, st] -> bar.sync -> MMA layer l+1
+// and the tensor pipe interleaves the slots' MMAs (no head-of-line blocking).
 template <int W, int LC, int H0C, int H1C, int MODE>
-__global__ void __launch_bounds__((TcPlan<W>::NSLOT * TcPlan<W>::WPS + 1) * 32, 1)
+__global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     k_fwd_tc(const TcParams p) {
   const int L = LC ? LC : p.L;
   const int NH = LC ? ((H0C ? 1 : 0) + (H1C ? 1 : 0)) : p.nh;
   const int h0 = LC ? H0C - 1 : (p.nh > 0 ? p.ha0 - 1 : -1);
   const int h1 = LC ? H1C - 1 : (p.nh > 1 ? p.ha1 - 1 : -1);
   constexpr int NSLOT = TcPlan<W>::NSLOT, WPS = TcPlan<W>::WPS, COLS = TcPlan<W>::COLS;
-  constexpr int NEPI = NSLOT * WPS;        // epilogue warps
+  constexpr int NEPI = NSLOT * WPS;        // warps
   constexpr int CPT = W * 4 / WPS;         // accumulator columns per thread
   constexpr int NCH = CPT / 32;            // 32-column chunks per thread
   static_assert(CPT % 32 == 0, "chunking");
   static_assert(NSLOT * W + NSLOT * (W / 2) <= COLS, "TMEM plan");
+  static_assert(NSLOT <= 7, "named barriers 1..NSLOT and 8..");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
-  // bars[0] weights, bars[1..NSLOT] a_full, bars[1+NSLOT..2 NSLOT] acc_full
+  // bars[0] weights, bars[1 + s] acc_full of slot s
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * NSLOT);  // 16-B aligned
   float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [NSLOT][2][4][32][3] head partials
   uint32_t* ctr = reinterpret_cast<uint32_t*>(xch + NSLOT * 2 * 4 * 32 * 3);  // [NEPI][12]
@@ -173,17 +200,18 @@ __global__ void __launch_bounds__((TcPlan<W>::NSLOT * TcPlan<W>::WPS + 1) * 32, 
   auto y_stage = [&](int s, int b) { return yst + (size_t)(2 * s + b) * kTile; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto a_full = [&](int s) { return smem_u32(bars + 1 + s); };
-  auto acc_full = [&](int s) { return smem_u32(bars + 1 + NSLOT + s); };
+#ifdef NB_TRACE
+  unsigned long long tr_i = 0;
+#endif
+  auto acc_full = [&](int s) { return smem_u32(bars + 1 + s); };
   auto acc_col = [](int s) { return (uint32_t)(s * W); };
   auto a_col = [](int s) { return (uint32_t)(NSLOT * W + s * (W / 2)); };
 
-  if (warp == NEPI) {
+  if (warp == 0) {
     if (lane == 0) {
       const uint32_t w_bar = smem_u32(bars);
       mbar_init(w_bar, 1);
       for (int s = 0; s < NSLOT; ++s) {
-        mbar_init(a_full(s), WPS * 32);
         mbar_init(acc_full(s), 1);
         mbar_init(stage_bar(s, 0), 1);
         mbar_init(stage_bar(s, 1), 1);
@@ -208,213 +236,217 @@ __global__ void __launch_bounds__((TcPlan<W>::NSLOT * TcPlan<W>::WPS + 1) * 32, 
   const int64_t n = p.a.n;
   const int64_t G = gridDim.x;
 
-  if (warp == NEPI) {
-    // ---------------- MMA issuer (one thread) ----------------
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(128, W);
-      uint32_t ph[NSLOT];
-#pragma unroll
-      for (int s = 0; s < NSLOT; ++s) ph[s] = 0u;
-      for (int64_t jp = 0;; jp += NSLOT) {
-        const int64_t t0 = blockIdx.x + jp * G;
-        if (t0 >= p.num_tiles) break;
-#pragma unroll
-        for (int l = 0; l < (LC ? LC : kMaxLayers); ++l) {
-          if (!LC && l >= L) break;
-          const uint32_t K = l == 0 ? (uint32_t)kEncK : (uint32_t)W;
-          const uint32_t sbo = (K / 8u) * 128u;
-          const uint32_t bimg = sbase + p.pl.off_w[l];
-#pragma unroll
-          for (int s = 0; s < NSLOT; ++s) {
-            if (t0 + s * G >= p.num_tiles) continue;
-            mbar_wait(a_full(s), ph[s]);
-            ph[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t d = tmem + acc_col(s);
-            const uint32_t a = tmem + a_col(s);
-#pragma unroll
-            for (uint32_t kk = 0; kk < K / 16u; ++kk)
-              mma_ts(d, a + kk * 8u, make_sdesc(bimg + kk * 256u, 128u, sbo), idesc, kk > 0u);
-            mma_commit(acc_full(s));
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- epilogue warps ----------------
-    const int s = warp / WPS;              // tile slot
-    const int qw = warp & 3;               // TMEM lane quarter
-    const int half = (warp % WPS) >> 2;    // column half (WPS == 8)
-    const int col0 = half * CPT;
-    const bool lead = half == 0;           // owns input staging and classification
-    const bool issuer = (warp % WPS) == 0 && lane == 0;  // stages the slot's records
-    const int rit = qw * 32 + lane;        // row within the tile
-    const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
-    const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
-    const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
-    const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
-    const float* cst = reinterpret_cast<const float*>(smem + p.pl.off_c);
-    const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]) + col0;
-    const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]) + col0;
-    uint32_t* cnt = ctr + warp * 12;       // per-warp counters in shared memory
-    uint32_t key[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    uint32_t ph = 0;
-    const int nl = 1 + NH;
-    const uint32_t named_bar = 1u + (uint32_t)(s * 4 + qw);
-    const int d0 = p.d0;
+  const int s = warp / WPS;              // tile slot
+  const int qw = warp & 3;               // TMEM lane quarter
+  const int half = (warp % WPS) >> 2;    // column half (WPS == 8)
+  const int col0 = half * CPT;
+  const bool lead = half == 0;           // owns input staging and classification
+  const bool mma_warp = (warp % WPS) == 0;             // issues the slot's MMAs
+  const bool issuer = mma_warp && lane == 0;           // stages the slot's records
+  const int rit = qw * 32 + lane;        // row within the tile
+  const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
+  const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
+  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
+  const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
+  const float* cst = reinterpret_cast<const float*>(smem + p.pl.off_c);
+  const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]) + col0;
+  const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]) + col0;
+  uint32_t* cnt = ctr + warp * 12;       // per-warp counters in shared memory
+  uint32_t key[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  uint32_t ph = 0;
+  const int nl = 1 + NH;
+  const uint32_t slot_bar = 1u + (uint32_t)s;              // all WPS warps of the slot
+  const uint32_t half_bar = 8u + (uint32_t)(s * 4 + qw);   // the 2 warps of a row quarter
+  const int d0 = p.d0;
+  const uint32_t idesc = make_idesc_bf16(128, W);
 
-    // Records of a full tile are staged into shared memory by the TMA bulk-copy
-    // engine one tile ahead (double-buffered per slot); a ragged last tile is
-    // read directly.
-    auto full_tile = [&](int64_t t) { return (t + 1) * kTile <= n; };
-    auto stage_issue = [&](int64_t t, int b) {
-      if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
-      const uint32_t qb = (uint32_t)(kTile * d0 * 4);
-      const uint32_t bar = stage_bar(s, b);
-      mbar_arrive_expect_tx(bar, qb + (MODE != kForward ? (uint32_t)kTile : 0u));
-      bulk_g2s(smem_u32(q_stage(s, b)), p.a.q + t * kTile * d0, qb, bar);
-      if (MODE != kForward) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
-    };
-    uint32_t sph[2] = {0u, 0u};
-    int ycur = 0;
-    // encode the slot's i-th tile t into the slot's TMEM A region
-    auto put_input = [&](int64_t t, int i) {
-      if (lead) {
-        float x[8];
-        const int b = i & 1;
-        if (full_tile(t)) {
-          mbar_wait(stage_bar(s, b), sph[b]);
-          sph[b] ^= 1u;
-          const float* qs = q_stage(s, b) + rit * d0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
-          ycur = MODE != kForward ? (int)y_stage(s, b)[rit] : 0;
+  // all warps of the slot have stored the next A operand: the lead warp issues
+  // layer l's MMAs (one elected lane) and commits them to acc_full[s]
+  auto sync_and_issue = [&](int l) {
+    tc_fence_before();
+    asm volatile("bar.sync %0, %1;" ::"r"(slot_bar), "n"(WPS * 32) : "memory");
+    if (mma_warp) {
+      if (lane == 0) NB_TR(1 + s, NB_EV(0, s, l));
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t d = tmem + acc_col(s);
+        const uint32_t a = tmem + a_col(s);
+        if (l == 0) {
+          mma_ts(d, a, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u), idesc, 0u);
         } else {
-          const int64_t r = t * kTile + rit;
-          const bool v = r < n;
+          const uint64_t bdesc = make_sdesc(sbase + p.pl.off_w[l], 128u, (W / 8u) * 128u);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
-          ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
+          for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
+            mma_ts(d, a + kk * 8u, bdesc + (uint64_t)(kk * 16u), idesc, kk > 0u);
         }
-        uint32_t c[8];
-        encode_cols(x, d0, c);
-        tmem_st8(trow + a_col(s), c);
-        tmem_wait_st();
+        mma_commit(acc_full(s));
       }
-      tc_fence_before();
-      mbar_arrive(a_full(s));
-    };
+      __syncwarp();
+      if (lane == 0) NB_TR(1 + s, NB_EV(1, s, l));
+    }
+  };
 
-    int64_t tile = blockIdx.x + (int64_t)s * G;
-    stage_issue(tile, 0);
-    stage_issue(tile + NSLOT * G, 1);
-    int i_tile = 0;
-    if (tile < p.num_tiles) put_input(tile, 0);
-    uint32_t par = 0;
-    while (tile < p.num_tiles) {
-      const int64_t next = tile + NSLOT * G;
-      float z0 = lead ? bout : 0.f, z1 = 0.f;
-      float e0a = (lead && NH > 0) ? cst[0] : 0.f, e0b = 0.f;
-      float e1a = (lead && NH > 1) ? cst[1] : 0.f, e1b = 0.f;
+  // Records of a full tile are staged into shared memory by the TMA bulk-copy
+  // engine one tile ahead (double-buffered per slot); a ragged last tile is
+  // read directly.
+  auto full_tile = [&](int64_t t) { return (t + 1) * kTile <= n; };
+  auto stage_issue = [&](int64_t t, int b) {
+    if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
+    const uint32_t qb = (uint32_t)(kTile * d0 * 4);
+    const uint32_t bar = stage_bar(s, b);
+    mbar_arrive_expect_tx(bar, qb + (MODE != kForward ? (uint32_t)kTile : 0u));
+    bulk_g2s(smem_u32(q_stage(s, b)), p.a.q + t * kTile * d0, qb, bar);
+    if (MODE != kForward) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
+  };
+  uint32_t sph[2] = {0u, 0u};
+  int ycur = 0;
+  // encode the slot's i-th tile t into the slot's TMEM A region, then issue layer 0
+  auto put_input = [&](int64_t t, int i) {
+    if (lead) {
+      float x[8];
+      const int b = i & 1;
+      if (full_tile(t)) {
+        mbar_wait(stage_bar(s, b), sph[b]);
+        sph[b] ^= 1u;
+        const float* qs = q_stage(s, b) + rit * d0;
 #pragma unroll
-      for (int l = 0; l < (LC ? LC : kMaxLayers); ++l) {
-        if (!LC && l >= L) break;
-        mbar_wait(acc_full(s), ph);
-        ph ^= 1u;
-        tc_fence_after();
-        // layer 0 of this tile has consumed its staged input: refill that buffer
-        if (l == 0) stage_issue(next + NSLOT * G, i_tile & 1);
-        const bool last = (l == L - 1);
-        const float* bias = bias_all + l * W + col0;
-        uint32_t v[CPT];
+        for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
+        ycur = MODE != kForward ? (int)y_stage(s, b)[rit] : 0;
+      } else {
+        const int64_t r = t * kTile + rit;
+        const bool v = r < n;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
+        ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
+      }
+      uint32_t c[8];
+      encode_cols(x, d0, c);
+      tmem_st8(trow + a_col(s), c);
+      tmem_wait_st();
+    }
+    if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(5, s, 0));
+    sync_and_issue(0);
+  };
+
+  int64_t tile = blockIdx.x + (int64_t)s * G;
+  stage_issue(tile, 0);
+  stage_issue(tile + NSLOT * G, 1);
+  int i_tile = 0;
+  if (tile < p.num_tiles) put_input(tile, 0);
+  uint32_t par = 0;
+  while (tile < p.num_tiles) {
+    const int64_t next = tile + NSLOT * G;
+    float z0 = lead ? bout : 0.f, z1 = 0.f;
+    float e0a = (lead && NH > 0) ? cst[0] : 0.f, e0b = 0.f;
+    float e1a = (lead && NH > 1) ? cst[1] : 0.f, e1b = 0.f;
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : kMaxLayers); ++l) {
+      if (!LC && l >= L) break;
+      mbar_wait(acc_full(s), ph);
+      if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(2, s, l));
+      ph ^= 1u;
+      tc_fence_after();
+      // layer 0 of this tile has consumed its staged input: refill that buffer
+      if (l == 0) stage_issue(next + NSLOT * G, i_tile & 1);
+      const bool last = (l == L - 1);
+      const float* bias = bias_all + l * W + col0;
+      // All of a layer's loads are issued before one wait when registers allow.
+      constexpr bool kAllLoads = NEPI <= 16;
+      uint32_t v[kAllLoads ? CPT : 32];
+      if (kAllLoads) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
           tmem_ld32(trow + acc_col(s) + (uint32_t)(col0 + 32 * c),
-                    *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+                    *reinterpret_cast<uint32_t(*)[32]>(v + (kAllLoads ? 32 * c : 0)));
         tmem_wait_ld();
+      }
+      if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(3, s, l));
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          float* t = reinterpret_cast<float*>(v + 32 * c);
+      for (int c = 0; c < NCH; ++c) {
+        if (!kAllLoads) {
+          tmem_ld32(trow + acc_col(s) + (uint32_t)(col0 + 32 * c),
+                    *reinterpret_cast<uint32_t(*)[32]>(v));
+          tmem_wait_ld();
+        }
+        float* t = reinterpret_cast<float*>(v + (kAllLoads ? 32 * c : 0));
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
-            add2(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
-            add2(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
-          }
-          if (!last) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
-            tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
-          }
-          if (l == h0 || l == h1 || last) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
-            const int o = 32 * c;
-            if (l == h0) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) fma2(e0a, e0b, t[i], t[i + 1], u0[o + i], u0[o + i + 1]);
-            }
-            if (l == h1) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) fma2(e1a, e1b, t[i], t[i + 1], u1[o + i], u1[o + i + 1]);
-            }
-            if (last) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) fma2(z0, z1, t[i], t[i + 1], wout[o + i], wout[o + i + 1]);
-            }
-          }
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
+          add2(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
+          add2(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
         }
         if (!last) {
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(a_full(s));
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+          tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
         }
-      }
-      // this tile's label, then stage the slot's next input into TMEM
-      const int ythis = ycur;
-      ++i_tile;
-      if (next < p.num_tiles) put_input(next, i_tile);
-      float z = z0 + z1;
-      float e[2] = {e0a + e0b, e1a + e1b};
-      if (WPS == 8) {  // combine the two column halves of each row
-        float* xb = xch + ((((size_t)s * 2 + par) * 4 + qw) * 32 + lane) * 3;
-        if (!lead) {
-          xb[0] = z;
-          xb[1] = e[0];
-          xb[2] = e[1];
-        }
-        asm volatile("bar.sync %0, %1;" ::"r"(named_bar), "n"(64) : "memory");
-        if (lead) {
-          z += xb[0];
-          e[0] += xb[1];
-          e[1] += xb[2];
-        }
-        par ^= 1u;
-      }
-      if (lead) {
-        const int64_t r = tile * kTile + rit;
-        const bool valid = r < n;
-        if (MODE == kForward) {
-          if (valid) {
-            p.a.logits[r * nl] = z;
-            if (NH > 0) p.a.logits[r * nl + 1] = e[0];
-            if (NH > 1) p.a.logits[r * nl + 2] = e[1];
-            if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
-            if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
+        if (l == h0 || l == h1 || last) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
+          const int o = 32 * c;
+          if (l == h0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2(e0a, e0b, t[i], t[i + 1], u0[o + i], u0[o + i + 1]);
           }
-        } else {
-          classify_row_smem<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+          if (l == h1) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2(e1a, e1b, t[i], t[i + 1], u1[o + i], u1[o + i + 1]);
+          }
+          if (last) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2(z0, z1, t[i], t[i + 1], wout[o + i], wout[o + i + 1]);
+          }
         }
       }
-      tile = next;
+      if (!last) {
+        tmem_wait_st();
+        if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(4, s, l));
+        sync_and_issue(l + 1);
+      }
     }
-    if (MODE != kForward && lead) flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
+    // this tile's label, then stage the slot's next input into TMEM
+    const int ythis = ycur;
+    ++i_tile;
+    if (next < p.num_tiles) put_input(next, i_tile);
+    float z = z0 + z1;
+    float e[2] = {e0a + e0b, e1a + e1b};
+    if (WPS == 8) {  // combine the two column halves of each row
+      float* xb = xch + ((((size_t)s * 2 + par) * 4 + qw) * 32 + lane) * 3;
+      if (!lead) {
+        xb[0] = z;
+        xb[1] = e[0];
+        xb[2] = e[1];
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "n"(64) : "memory");
+      if (lead) {
+        z += xb[0];
+        e[0] += xb[1];
+        e[1] += xb[2];
+      }
+      par ^= 1u;
+    }
+    if (lead) {
+      const int64_t r = tile * kTile + rit;
+      const bool valid = r < n;
+      if (MODE == kForward) {
+        if (valid) {
+          p.a.logits[r * nl] = z;
+          if (NH > 0) p.a.logits[r * nl + 1] = e[0];
+          if (NH > 1) p.a.logits[r * nl + 2] = e[1];
+          if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
+          if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
+        }
+      } else {
+        classify_row_smem<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+      }
+    }
+    tile = next;
   }
+  if (MODE != kForward && lead) flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
   tc_fence_before();
   __syncthreads();
-  if (warp == NEPI) {
+  if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<COLS>(tmem);
   }
@@ -426,6 +458,12 @@ bool tc_supported(const nb_desc& d) {
   if (d.hidden_layers < 1 || d.hidden_layers > kMaxLayers) return false;
   return true;
 }
+
+// NB_TRACE builds: device buffer set by nb_debug_set_trace (tools/trace_fwd.py).
+static unsigned long long* g_trace_buffer = nullptr;
+#ifdef NB_TRACE
+extern "C" void nb_debug_set_trace(void* dev_buf) { g_trace_buffer = (unsigned long long*)dev_buf; }
+#endif
 
 template <int W, int LC, int H0C, int H1C, int MODE>
 static cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
@@ -440,6 +478,7 @@ static cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   p.ha0 = m->d.head_after[0];
   p.ha1 = m->d.head_after[1];
   p.num_tiles = (a.n + kTile - 1) / kTile;
+  p.trace = g_trace_buffer;
   if (p.num_tiles == 0) return cudaSuccess;
   // weights | barriers + tmem slot | head-partial exchange | counters | staging;
   // requesting >= 116 KB also forces one CTA per SM (TMEM is allocated whole)
@@ -451,7 +490,7 @@ static cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
-  kern<<<grid, (NSLOT * WPS + 1) * 32, smem, st>>>(p);
+  kern<<<grid, NSLOT * WPS * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -113,6 +113,157 @@ __global__ void k_mma(int iters, unsigned long long* out) {
   if (warp == 0) tmem_dealloc<512>(tslot);
 }
 
+
+// MMA throughput while other warps stream tcgen05.ld / tcgen05.st traffic
+template <int N, int LDW, bool ST>
+__global__ void k_mma_contended(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(smem_u32(&tslot));
+  if (threadIdx.x == 32) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_barrier_init();
+    stop = 0;
+  }
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3F80;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, N);
+    const uint32_t sb = smem_u32(smem);
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t kk = i & 3;
+      mma_ts(tm, tm + 128 + kk * 8, make_sdesc(sb + kk * 256, 128, 1024), idesc, kk > 0);
+    }
+    mma_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    unsigned long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    stop = 1;
+  } else if (warp >= 1 && warp <= LDW) {
+    const uint32_t t = tm + ((uint32_t)((warp & 3) * 32) << 16) + 192 + (uint32_t)(((warp - 1) >> 2) * 64);
+    uint32_t acc = 0;
+    while (!stop) {
+      uint32_t v[32];
+      tmem_ld32(t, v);
+      tmem_wait_ld();
+      if (ST) {
+        uint32_t r[16];
+        for (int j = 0; j < 16; ++j) r[j] = v[j] ^ v[j + 16];
+        tmem_st16(t + 32, r);
+        tmem_wait_st();
+      }
+      acc ^= v[3];
+    }
+    if (acc == 0x1234567) out[1000] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tslot);
+}
+
+
+// latency: issue NK MMAs (one layer) + commit, wait on the mbarrier; repeat
+template <int N, int NK>
+__global__ void k_mma_latency(int reps, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(smem_u32(&tslot));
+  if (threadIdx.x == 32) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3F80;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, N);
+    const uint32_t sb = smem_u32(smem);
+    unsigned long long t0 = clock64(), tissue = 0;
+    for (int r = 0; r < reps; ++r) {
+      unsigned long long a = clock64();
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk)
+        mma_ts(tm, tm + 256 + kk * 8, make_sdesc(sb + kk * 256, 128, NK * 256), idesc, kk > 0);
+      mma_commit(smem_u32(&bar));
+      tissue += clock64() - a;
+      mbar_wait(smem_u32(&bar), r & 1);
+      tc_fence_after();
+    }
+    unsigned long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    out[200 + blockIdx.x] = tissue;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tslot);
+}
+
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+// same as k_mma_latency but the whole warp runs the loop; one elected lane issues
+template <int N, int NK>
+__global__ void k_mma_latency_warp(int reps, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(smem_u32(&tslot));
+  if (threadIdx.x == 32) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3F80;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tslot;
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, N);
+    const uint32_t sb = smem_u32(smem);
+    const uint64_t d0 = make_sdesc(sb, 128, NK * 256);
+    unsigned long long t0 = clock64(), tissue = 0;
+    for (int r = 0; r < reps; ++r) {
+      unsigned long long a = clock64();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk)
+          mma_ts(tm, tm + 256 + kk * 8, d0 + (uint64_t)(kk * 16), idesc, kk > 0);
+        mma_commit(smem_u32(&bar));
+      }
+      __syncwarp();
+      tissue += clock64() - a;
+      mbar_wait(smem_u32(&bar), r & 1);
+      tc_fence_after();
+    }
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      out[blockIdx.x] = t1 - t0;
+      out[200 + blockIdx.x] = tissue;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tslot);
+}
+
 static double median_cycles(unsigned long long* d, int n) {
   unsigned long long h[1024];
   cudaMemcpy(h, d, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
@@ -154,6 +305,37 @@ int main() {
   RUN_MMA(64, false, 1) RUN_MMA(128, false, 1) RUN_MMA(256, false, 1)
   RUN_MMA(32, true, 2) RUN_MMA(32, true, 4) RUN_MMA(64, true, 2) RUN_MMA(64, true, 4) RUN_MMA(128, true, 2)
   RUN_MMA(64, false, 2) RUN_MMA(64, false, 4) RUN_MMA(32, false, 4)
+#define RUN_C(NN, LW, ST)                                                                      \
+  {                                                                                           \
+    cudaFuncSetAttribute(k_mma_contended<NN, LW, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024); \
+    k_mma_contended<NN, LW, ST><<<grid, 544, 64 * 1024>>>(iters, d);                          \
+    cudaError_t e = cudaDeviceSynchronize();                                                  \
+    double c = median_cycles(d, grid);                                                        \
+    printf("mma ts N=%3d K=16 SBO=1024 with %2d ld warps st=%d: %.1f cycles/instr %s\n", NN, LW, (int)ST, c / iters, cudaGetErrorString(e)); \
+  }
+  RUN_C(64, 0, false) RUN_C(64, 4, false) RUN_C(64, 16, false) RUN_C(64, 16, true) RUN_C(128, 0, false) RUN_C(128, 16, true)
+#define RUN_L(NN, NK)                                                                      \
+  {                                                                                           \
+    cudaFuncSetAttribute(k_mma_latency<NN, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024); \
+    k_mma_latency<NN, NK><<<grid, 128, 64 * 1024>>>(500, d);                          \
+    cudaError_t e = cudaDeviceSynchronize();                                                  \
+    double c = median_cycles(d, grid);                                                        \
+    unsigned long long hi[148]; cudaMemcpy(hi, d + 200, sizeof(hi), cudaMemcpyDeviceToHost); \
+    double is = 0; for (int i = 0; i < 148; ++i) is += hi[i]; is /= 148;                      \
+    printf("layer latency N=%3d K=%3d: %.1f cycles per (issue+commit+wait), issue part %.1f %s\n", NN, NK * 16, c / 500, is / 500, cudaGetErrorString(e)); \
+  }
+  RUN_L(64, 1) RUN_L(64, 4) RUN_L(128, 1) RUN_L(128, 8)
+#define RUN_LW(NN, NK)                                                                      \
+  {                                                                                           \
+    cudaFuncSetAttribute(k_mma_latency_warp<NN, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024); \
+    k_mma_latency_warp<NN, NK><<<grid, 128, 64 * 1024>>>(500, d);                          \
+    cudaError_t e = cudaDeviceSynchronize();                                                  \
+    double c = median_cycles(d, grid);                                                        \
+    unsigned long long hi[148]; cudaMemcpy(hi, d + 200, sizeof(hi), cudaMemcpyDeviceToHost); \
+    double is = 0; for (int i = 0; i < 148; ++i) is += hi[i]; is /= 148;                      \
+    printf("warp-elect layer latency N=%3d K=%3d: %.1f cycles, issue part %.1f %s\n", NN, NK * 16, c / 500, is / 500, cudaGetErrorString(e)); \
+  }
+  RUN_LW(64, 1) RUN_LW(64, 4) RUN_LW(128, 8)
   int clk;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("clock rate attr %d kHz\n", clk);
