@@ -181,6 +181,10 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   constexpr int NEPI = NSLOT * WPS;        // warps
   constexpr int CPT = W * 4 / WPS;         // accumulator columns per thread
   constexpr int NCH = CPT / 32;            // 32-column chunks per thread
+  // With enough registers all of a layer's loads are issued before one wait,
+  // and the next tile is staged as soon as the last layer's accumulator is in
+  // registers (its layer-0 MMA then overlaps this tile's output epilogue).
+  constexpr bool kAllLoads = NEPI <= 16;
   static_assert(CPT % 32 == 0, "chunking");
   static_assert(NSLOT * W + NSLOT * (W / 2) <= COLS, "TMEM plan");
   static_assert(NSLOT <= 7, "named barriers 1..NSLOT and 8..");
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   uint32_t par = 0;
   while (tile < p.num_tiles) {
     const int64_t next = tile + NSLOT * G;
+    int ythis = 0;
     float z0 = lead ? bout : 0.f, z1 = 0.f;
     float e0a = (lead && NH > 0) ? cst[0] : 0.f, e0b = 0.f;
     float e1a = (lead && NH > 1) ? cst[1] : 0.f, e1b = 0.f;
@@ -350,8 +355,6 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
       if (l == 0) stage_issue(next + NSLOT * G, i_tile & 1);
       const bool last = (l == L - 1);
       const float* bias = bias_all + l * W + col0;
-      // All of a layer's loads are issued before one wait when registers allow.
-      constexpr bool kAllLoads = NEPI <= 16;
       uint32_t v[kAllLoads ? CPT : 32];
       if (kAllLoads) {
 #pragma unroll
@@ -361,6 +364,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         tmem_wait_ld();
       }
       if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(3, s, l));
+      if (kAllLoads && last) {
+        // the accumulator is in registers and the last MMA has completed: stage
+        // the slot's next tile now so its layer-0 MMA overlaps this epilogue
+        ythis = ycur;
+        ++i_tile;
+        if (next < p.num_tiles) put_input(next, i_tile);
+      }
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         if (!kAllLoads) {
@@ -405,10 +415,11 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         sync_and_issue(l + 1);
       }
     }
-    // this tile's label, then stage the slot's next input into TMEM
-    const int ythis = ycur;
-    ++i_tile;
-    if (next < p.num_tiles) put_input(next, i_tile);
+    if (!kAllLoads) {
+      ythis = ycur;
+      ++i_tile;
+      if (next < p.num_tiles) put_input(next, i_tile);
+    }
     float z = z0 + z1;
     float e[2] = {e0a + e0b, e1a + e1b};
     if (WPS == 8) {  // combine the two column halves of each row
