@@ -71,6 +71,7 @@ def lib():
             "ora_num_params": (I64, [P]),
             "ora_forward": (None, [P, P, P, I64, I32, P]),
             "ora_loss_grad": (D, [P, P, P, P, I64, I64, D, D, P, P]),
+            "ora_loss_grad_mode": (D, [P, P, P, P, I64, I64, D, D, P, P, I32]),
             "ora_weighted_bce": (D, [D, I32, D, D]),
             "ora_adam": (None, [I64, P, P, P, I64, D, D, D, D, P]),
             "ora_alpha": (D, [I64, I64]),
@@ -160,16 +161,16 @@ def forward(a: Arch, theta, q, mode=FP64) -> np.ndarray:
     return out
 
 
-def loss_grad(a: Arch, theta, q, y, alpha, beta, n_global=None):
+def loss_grad(a: Arch, theta, q, y, alpha, beta, n_global=None, mode=FP64):
     th = _np(theta, np.float64)
     q = _np(q, np.float32)
     yy = _np(y, np.uint8)
     n = q.shape[0]
     g = np.zeros(num_params(a), np.float64)
     st = Stats()
-    loss = lib().ora_loss_grad(C.byref(a), _ptr(th), _ptr(q), _ptr(yy), n,
-                               n if n_global is None else n_global, alpha, beta, _ptr(g),
-                               C.byref(st))
+    loss = lib().ora_loss_grad_mode(C.byref(a), _ptr(th), _ptr(q), _ptr(yy), n,
+                                    n if n_global is None else n_global, alpha, beta, _ptr(g),
+                                    C.byref(st), mode)
     return loss, g, dict(loss=st.loss, tp=st.tp, fp=st.fp, fn=st.fn, tn=st.tn)
 
 

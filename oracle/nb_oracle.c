@@ -388,6 +388,7 @@ static void forward_one(const ora_arch* a, const offsets* of, const double* th, 
       if (mode == ORA_BF16_EMU) {
         float z = (float)s + (float)b[o];
         float rr = z > 0.0f ? z : 0.0f;
+        if (pre) pre[(int64_t)l * w + o] = (double)z;
         rl[o] = rr;
         hn[o] = (l < L - 1) ? (double)bf16_round(rr) : (double)rr;
       } else {
@@ -436,9 +437,13 @@ double ora_weighted_bce(double z, int32_t y, double alpha, double beta) {
   return y ? alpha * softplus(-z) : beta * softplus(z);
 }
 
-double ora_loss_grad(const ora_arch* a, const double* th, const float* q, const uint8_t* y,
-                     int64_t n, int64_t n_global, double alpha, double beta, double* grad,
-                     ora_stats* st) {
+/* Gradient of the loss of the network evaluated in `mode`: ORA_FP64 is the
+ * plain definition; ORA_BF16_EMU differentiates the bf16-precision forward of
+ * R33 (its rounded activations and fp32 pre-activations give the ReLU masks,
+ * bf16 weights propagate the deltas), the rest in fp64.                    */
+static double loss_grad_impl(const ora_arch* a, const double* th, const float* q,
+                             const uint8_t* y, int64_t n, int64_t n_global, double alpha,
+                             double beta, double* grad, ora_stats* st, int mode) {
   offsets of;
   param_offsets(a, &of);
   const int w = a->width, L = a->layers, d0 = a->d0;
@@ -454,7 +459,7 @@ double ora_loss_grad(const ora_arch* a, const double* th, const float* q, const 
   const double B = (double)n_global;
   for (int64_t i = 0; i < n; ++i) {
     double out[3];
-    forward_one(a, &of, th, q + i * d0, ORA_FP64, out, acts, pre);
+    forward_one(a, &of, th, q + i * d0, mode, out, acts, pre);
     const int yi = y[i] ? 1 : 0;
     const double wi = yi ? alpha : beta;
     /* output logit and its gradient dL/dz = w (sigmoid(z) - y) / B (a7) */
@@ -495,7 +500,11 @@ double ora_loss_grad(const ora_arch* a, const double* th, const float* q, const 
       if (l > 0) {
         for (int kk = 0; kk < in; ++kk) {
           double s = 0.0;
-          for (int o = 0; o < w; ++o) s += dz[o] * W[(int64_t)o * in + kk];
+          for (int o = 0; o < w; ++o) {
+            double wv = W[(int64_t)o * in + kk];
+            if (mode == ORA_BF16_EMU) wv = (double)bf16_round((float)wv);
+            s += dz[o] * wv;
+          }
           dh[kk] = s;
         }
       }
@@ -504,6 +513,18 @@ double ora_loss_grad(const ora_arch* a, const double* th, const float* q, const 
   free(acts); free(pre); free(dh); free(dz);
   if (st) { st->loss = loss; st->tp = tp; st->fp = fp; st->fn = fn; st->tn = tn; }
   return loss;
+}
+
+double ora_loss_grad(const ora_arch* a, const double* th, const float* q, const uint8_t* y,
+                     int64_t n, int64_t n_global, double alpha, double beta, double* grad,
+                     ora_stats* st) {
+  return loss_grad_impl(a, th, q, y, n, n_global, alpha, beta, grad, st, ORA_FP64);
+}
+
+double ora_loss_grad_mode(const ora_arch* a, const double* th, const float* q, const uint8_t* y,
+                          int64_t n, int64_t n_global, double alpha, double beta, double* grad,
+                          ora_stats* st, int32_t mode) {
+  return loss_grad_impl(a, th, q, y, n, n_global, alpha, beta, grad, st, mode);
 }
 
 /* ------------------------------------------------------------------------ */

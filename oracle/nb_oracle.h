@@ -70,6 +70,11 @@ void ora_forward(const ora_arch* a, const double* theta, const float* q, int64_t
 double ora_loss_grad(const ora_arch* a, const double* theta, const float* q,
                      const uint8_t* y, int64_t n, int64_t n_global, double alpha,
                      double beta, double* grad, ora_stats* stats);
+/* Same for the network evaluated in `mode` (ORA_BF16_EMU: gradient of the
+ * bf16-precision forward of R33, the kernel's arithmetic). */
+double ora_loss_grad_mode(const ora_arch* a, const double* theta, const float* q,
+                          const uint8_t* y, int64_t n, int64_t n_global, double alpha,
+                          double beta, double* grad, ora_stats* stats, int32_t mode);
 /* Per-sample loss term only (for KATs): w * softplus(+-z). */
 double ora_weighted_bce(double z, int32_t y, double alpha, double beta);
 

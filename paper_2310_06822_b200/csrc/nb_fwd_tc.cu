@@ -326,6 +326,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
       uint32_t c[8];
       encode_cols(x, d0, c);
       tmem_st8(trow + a_col(s), c);
+      if (MODE == kTrain) {  // layer-1 input image for the dW GEMM
+        uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(16);
+#pragma unroll
+        for (int fg = 0; fg < 2; ++fg)
+          *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+              make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+      }
       tmem_wait_st();
     }
     if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(5, s, 0));
@@ -385,11 +392,19 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           add2(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
           add2(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
         }
-        if (!last) {
+        if (!last || MODE == kTrain) {
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
-          tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
+          if (!last) tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
+          if (MODE == kTrain) {  // h_{l+1} image (activations kept for back-propagation)
+            uint8_t* base = p.a.tr.h_img[l] + tile * img_tile_bytes(W);
+            const int fg0 = (col0 + 32 * c) / 8;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<uint4*>(base + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                  make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
         if (l == h0 || l == h1 || last) {
 #pragma unroll
@@ -448,13 +463,49 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
           if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
         }
+      } else if (MODE == kTrain) {
+        // Eq. (1): w = alpha if y else beta; term w softplus(-+z);
+        // dL/dz = w (sigmoid(z) - y) / B; exit heads add the same term
+        const float yf = (float)ythis;
+        const float w = valid ? (ythis ? p.a.tr.alpha : p.a.tr.beta) : 0.f;
+        auto sp = [](float u) { return fmaxf(u, 0.f) + log1pf(__expf(-fabsf(u))); };
+        float lsum = w * sp(ythis ? -z : z);
+        const float gz = w * (1.f / (1.f + __expf(-z)) - yf) * p.a.tr.inv_b;
+        float ge[2] = {0.f, 0.f};
+        for (int k = 0; k < NH; ++k) {
+          lsum += w * sp(ythis ? -e[k] : e[k]);
+          ge[k] = w * (1.f / (1.f + __expf(-e[k])) - yf) * p.a.tr.inv_b;
+        }
+        const int64_t r3 = r * 3;
+        if (valid) {
+          p.a.tr.g32[r3] = gz;
+          p.a.tr.g32[r3 + 1] = ge[0];
+          p.a.tr.g32[r3 + 2] = ge[1];
+        }
+        uint8_t* hb = p.a.tr.hd_img + tile * img_tile_bytes(8) + (rit / 8) * 128 + (rit % 8) * 16;
+        *reinterpret_cast<uint4*>(hb) = make_uint4(pack_bf16x2(gz, ge[0]), pack_bf16x2(ge[1], 0.f), 0u, 0u);
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xFFFFFFFFu, lsum, o);
+        const bool pred = z >= 0.f, yy = ythis != 0;
+        const uint32_t c0 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
+        const uint32_t c1 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
+        const uint32_t c2 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && yy));
+        const uint32_t c3 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
+        if (lane == 0) {
+          atomicAdd(p.a.tr.loss, (double)lsum * (double)p.a.tr.inv_b);
+          cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
+        }
       } else {
         classify_row_smem<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
       }
     }
     tile = next;
   }
-  if (MODE != kForward && lead) flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
+  if ((MODE == kCalibrate || MODE == kScore) && lead)
+    flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
+  if (MODE == kTrain && lead && lane == 0) {
+    for (int i = 0; i < 4; ++i)
+      if (cnt[i]) atomicAdd(p.a.tr.stats + i, (unsigned long long)cnt[i]);
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -509,6 +560,7 @@ template <int W, int LC, int H0C, int H1C>
 static cudaError_t launch_tc_modes(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
   if (mode == kForward) return launch_tc_wm<W, LC, H0C, H1C, kForward>(m, a, st);
   if (mode == kCalibrate) return launch_tc_wm<W, LC, H0C, H1C, kCalibrate>(m, a, st);
+  if (mode == kTrain) return launch_tc_wm<W, LC, H0C, H1C, kTrain>(m, a, st);
   return launch_tc_wm<W, LC, H0C, H1C, kScore>(m, a, st);
 }
 

@@ -92,7 +92,22 @@ struct nb_grid {
 namespace nb {
 
 // ---- launchers (each returns cudaGetLastError of its launch) ---------------
-enum Mode { kForward = 0, kCalibrate = 1, kScore = 2 };
+enum Mode { kForward = 0, kCalibrate = 1, kScore = 2, kTrain = 3 };
+
+// Training-mode outputs of the forward kernel (bf16 training).
+// "Row-tile images": per 128-row tile, a [F features][128 rows] bf16 matrix in
+// UMMA MN-major no-swizzle core-matrix order,
+//   byte(r, f) = ((f / 8) * 16 + r / 8) * 128 + (r % 8) * 16 + (f % 8) * 2,
+// tile t at t * F * 256 bytes; consumed directly by the dW GEMM (bulk copy).
+struct TrainArgs {
+  uint8_t* x_img;                // encoded layer-1 input, F = 16
+  uint8_t* h_img[kMaxLayers];    // h_l (post-ReLU, bf16), F = w, l = 1..L
+  uint8_t* hd_img;               // [dL/dz, dL/de_1, dL/de_2, 0..] bf16, F = 8
+  float* g32;                    // fp32 [n][3]: dL/dz, dL/de_1, dL/de_2
+  float alpha, beta, inv_b;      // Eq. (1) weights, 1 / n_global
+  double* loss;
+  unsigned long long* stats;     // batch tp fp fn tn at z >= 0
+};
 
 struct FwdArgs {
   const float* q;
@@ -104,7 +119,10 @@ struct FwdArgs {
   unsigned long long* counts;
   unsigned int* keys;
   unsigned int* flags;
+  TrainArgs tr;
 };
+
+__host__ __device__ constexpr int64_t img_tile_bytes(int features) { return (int64_t)features * 256; }
 
 cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s);
 cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t s);

@@ -1,14 +1,501 @@
-// nb_train_tc.cu — bf16 training step on tcgen05 (hot-path rows a7-a9).
-// Placeholder until the tensor-core backward lands: reports unsupported.
+// nb_train_tc.cu — bf16 training step on tcgen05 tensor cores (rows a7-a9).
+//
+//  1. forward in kTrain mode (nb_fwd_tc.cu): same arithmetic as inference;
+//     writes the row-tile images of the encoded input X and of h_1..h_L, and
+//     dL/dz, dL/de_k of Eq. (1) (head terms P:261) per row.
+//  2. k_bwd_tc: per 128-row tile, back-propagation through the hidden layers
+//     delta_L = (dL/dz w_out + sum_k dL/de_k u_k [l_k = L]) * [h_L > 0],
+//     delta_{l-1} = (delta_l W_l + heads) * [h_{l-1} > 0]   (ReLU'(0) = 0, R25)
+//     as tcgen05.mma with A = delta_l (TMEM) and B = W_l read MN-major from the
+//     same shared-memory weight image the forward uses; writes delta images.
+//  3. k_dw_tc: dW_l = delta_l^T [h_{l-1} | 1] summed over row tiles with
+//     tcgen05.mma (A, B both MN-major from row-tile images; the constant "ones"
+//     block gives db_l = sum delta_l), per-CTA partials in fp32.
+//  4. k_dw_reduce: fixed-order sum of the CTA partials into the canonical
+//     gradient blob (deterministic); then NCCL allreduce, Adam, bf16 re-pack
+//     (nb_api.cu).
+#include <cuda_bf16.h>
+
+#include "nb_device.cuh"
 #include "nb_internal.cuh"
 
 namespace nb {
 
-bool train_tc_supported(const nb_desc&) { return false; }
-size_t train_tc_scratch_bytes(const nb_model*, int64_t) { return 0; }
-cudaError_t launch_train_tc(nb_model*, const float*, const uint8_t*, int64_t, int64_t, float,
-                            float, cudaStream_t) {
-  return cudaErrorNotSupported;
+constexpr int kDwMaxN = 256;  // features per dW MMA (plus the 16-wide ones block)
+
+// ---------------------------------------------------------------------------
+// backward chain
+// ---------------------------------------------------------------------------
+struct BwdParams {
+  const uint8_t* packed;
+  PackLayout pl;
+  int L, nh, ha0, ha1;
+  int64_t n, num_tiles;
+  const uint8_t* h_img[kMaxLayers];  // h_1..h_L images (F = W)
+  uint8_t* d_img[kMaxLayers];        // delta_1..delta_L images (F = W)
+  const float* g32;                  // [n][3]
+};
+
+__device__ __forceinline__ uint32_t img_off(int r, int fg) {
+  return (uint32_t)((fg * 16 + r / 8) * 128 + (r % 8) * 16);
+}
+
+// NSLOT tiles in flight, 4 warps (one per TMEM lane quarter) per slot, each
+// thread owns one row and walks its W columns in 32-column chunks.
+template <int W>
+__global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
+  constexpr int NSLOT = 2, WPS = 4;
+  constexpr int COLS = (NSLOT * (W + W / 2) <= 256) ? 256 : 512;
+  static_assert(NSLOT * (W + W / 2) <= 512, "TMEM plan");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);  // [0] weights, [1+s] acc_full
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(smem_u32(bars), 1);
+      for (int s = 0; s < NSLOT; ++s) mbar_init(smem_u32(bars + 1 + s), 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(smem_u32(bars), p.pl.bytes);
+      for (uint32_t off = 0; off < p.pl.bytes; off += 32768u)
+        bulk_g2s(sbase + off, p.packed + off, min(32768u, p.pl.bytes - off), smem_u32(bars));
+    }
+    __syncwarp();
+    tmem_alloc<COLS>(smem_u32(tmem_slot));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  mbar_wait(smem_u32(bars), 0);
+
+  const int s = warp / WPS, qw = warp & 3, rit = qw * 32 + lane;
+  const bool mma_warp = (warp % WPS) == 0;
+  const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
+  const uint32_t acc = (uint32_t)(s * W), acol = (uint32_t)(NSLOT * W + s * (W / 2));
+  const uint32_t acc_full = smem_u32(bars + 1 + s);
+  const uint32_t slot_bar = 1u + (uint32_t)s;
+  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout);
+  const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]);
+  const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]);
+  const int h0 = p.nh > 0 ? p.ha0 : -1, h1 = p.nh > 1 ? p.ha1 : -1;  // 1-based layers
+  // B = W_l^T: the K-major [out][in] image read MN-major (MN = in, K = out)
+  const uint32_t idesc = make_idesc_bf16(128, W, 0, 1);
+  uint32_t ph = 0;
+  const int64_t G = gridDim.x;
+
+  for (int64_t tile = blockIdx.x + (int64_t)s * G; tile < p.num_tiles; tile += NSLOT * G) {
+    const int64_t r = tile * kTile + rit;
+    const bool valid = r < p.n;
+    const float gz = valid ? p.g32[r * 3] : 0.f;
+    const float ge0 = valid ? p.g32[r * 3 + 1] : 0.f, ge1 = valid ? p.g32[r * 3 + 2] : 0.f;
+    // l (1-based) runs L .. 1; the value in flight is dL/dh_l
+    for (int l = p.L; l >= 1; --l) {
+      uint32_t v[32];
+      const uint8_t* hrow = p.h_img[l - 1] + tile * img_tile_bytes(W);
+      uint8_t* drow = p.d_img[l - 1] + tile * img_tile_bytes(W);
+      if (l < p.L) {
+        mbar_wait(acc_full, ph);
+        ph ^= 1u;
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < W / 32; ++c) {
+        if (l < p.L) {
+          tmem_ld32(trow + acc + 32u * c, v);
+          tmem_wait_ld();
+        }
+        float g[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = 32 * c + i;
+          float d = (l < p.L) ? __uint_as_float(v[i]) : gz * wout[j];
+          if (l == h0) d = fmaf(ge0, u0[j], d);
+          if (l == h1) d = fmaf(ge1, u1[j], d);
+          g[i] = d;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 hv = *reinterpret_cast<const uint4*>(hrow + img_off(rit, 4 * c + q));
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 8 * q + 2 * e;
+            const float m0 = (hw[e] & 0x7FFFu) ? g[i] : 0.f;           // h > 0 (h >= 0 by ReLU)
+            const float m1 = (hw[e] & 0x7FFF0000u) ? g[i + 1] : 0.f;
+            pk[4 * q + e] = pack_bf16x2(m0, m1);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(drow + img_off(rit, 4 * c + q)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        if (l >= 2) tmem_st16(trow + acol + 16u * c, pk);
+      }
+      if (l >= 2) {
+        // delta_l is in TMEM: MMA dL/dh_{l-1} = delta_l W_l (K = out of layer l)
+        tmem_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync %0, %1;" ::"r"(slot_bar), "n"(WPS * 32) : "memory");
+        if (mma_warp) {
+          tc_fence_after();
+          if (elect_one()) {
+            // MN-major: SBO = MN (in-group) stride 128 B, LBO = K (out-group) stride
+            const uint64_t bdesc =
+                make_sdesc(sbase + p.pl.off_w[l - 1], (W / 8u) * 128u, 128u);
+#pragma unroll
+            for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
+              mma_ts(tmem + acc, tmem + acol + kk * 8u, bdesc + (uint64_t)((kk * 32u * W) >> 4),
+                     idesc, kk > 0u);
+            mma_commit(acc_full);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<COLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dW GEMM: D[m][f] = sum over rows of A[m][row] B[f][row] for one job
+//   A = row-tile images with FA features (delta_l or the head-gradient image),
+//   B = row-tile images with FB features (h_{l-1}, X, ...) followed by the
+//       constant ones block (feature FB = 1) -> D[m][FB] = sum_rows A[m][row].
+// One CTA accumulates a contiguous range of tiles in TMEM (M = 128 rows of D;
+// rows >= FA are don't-care), then writes its fp32 partial.
+// ---------------------------------------------------------------------------
+struct DwJob {
+  const uint8_t* a_img;
+  int fa;        // features of the A image (rows of D that are meaningful)
+  int m_off;     // first A feature of this job (M half for w = 256)
+  const uint8_t* b_img;
+  int fb;        // features of the B image (<= 256)
+  float* partial;  // [gridDim.x][128][fb + 16]
+};
+
+__global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // A tile: 128 features (16 groups) x 128 rows = 32 KB; B tile + ones: (fb + 16) x 256 B
+  const uint32_t a_bytes = 128u * 256u;
+  const uint32_t b_bytes = (uint32_t)(j.fb + 16) * 256u;
+  const uint32_t stage = a_bytes + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * stage);  // [0,1] full, [2] mma done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sbase = smem_u32(smem);
+  const int N = j.fb + 16;
+  // ones block after each stage's B image: feature fb = 1.0 for every row
+  for (int st = 0; st < 2; ++st) {
+    uint8_t* ones = smem + st * stage + a_bytes + j.fb * 256;
+    for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) {
+      const int r = i / 16, f = i % 16;
+      *reinterpret_cast<uint16_t*>(ones + img_off(r, f / 8) + (f % 8) * 2) = f == 0 ? 0x3F80 : 0;
+    }
+    // rows of A beyond fa are read but never used: keep them finite
+    for (int i = threadIdx.x * 4; i < (int)a_bytes; i += blockDim.x * 4)
+      if (i >= j.fa * 256 || j.m_off > 0) *reinterpret_cast<uint32_t*>(smem + st * stage + i) = 0u;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(smem_u32(bars + i), 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(smem_u32(tmem_slot));
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int64_t per = (num_tiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = blockIdx.x * per, t1 = min(num_tiles, t0 + per);
+  const int fa_job = min(128, j.fa - j.m_off);
+  const uint32_t a_copy = (uint32_t)fa_job * 256u;  // bytes of this job's A features per tile
+  const uint32_t idesc = make_idesc_bf16(128, j.fb, 1, 1);
+  const uint32_t idesc1 = make_idesc_bf16(128, 16, 1, 1);
+  if (warp == 0) {
+    auto issue_copy = [&](int64_t t, int st) {
+      const uint32_t bar = smem_u32(bars + st);
+      mbar_arrive_expect_tx(bar, a_copy + (uint32_t)j.fb * 256u);
+      bulk_g2s(sbase + st * stage, j.a_img + t * img_tile_bytes(j.fa) + (int64_t)j.m_off * 256,
+               a_copy, bar);
+      bulk_g2s(sbase + st * stage + a_bytes, j.b_img + t * img_tile_bytes(j.fb),
+               (uint32_t)j.fb * 256u, bar);
+    };
+    uint32_t ph[2] = {0u, 0u}, done_ph = 0;
+    if (lane == 0 && t0 < t1) issue_copy(t0, 0);
+    for (int64_t t = t0; t < t1; ++t) {
+      const int st = (int)((t - t0) & 1);
+      if (lane == 0 && t + 1 < t1) {
+        // the other stage is free once the previous tile's MMAs completed
+        if (t > t0) {
+          mbar_wait(smem_u32(bars + 2), done_ph);
+          done_ph ^= 1u;
+        }
+        issue_copy(t + 1, st ^ 1);
+      }
+      mbar_wait(smem_u32(bars + st), ph[st]);
+      ph[st] ^= 1u;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t as = sbase + st * stage, bs = as + a_bytes;
+        // MN-major row-tile images: SBO (feature-group stride) 2048 B, LBO (row-group) 128 B
+        const uint64_t ad = make_sdesc(as, 128u, 2048u);
+        const uint64_t bd = make_sdesc(bs, 128u, 2048u);
+        const uint64_t od = make_sdesc(bs + (uint32_t)j.fb * 256u, 128u, 2048u);
+#pragma unroll
+        for (uint32_t kk = 0; kk < 8; ++kk) {
+          const uint32_t acc = (t > t0 || kk > 0) ? 1u : 0u;
+          mma_ss(tmem, ad + kk * 16u, bd + kk * 16u, idesc, acc);
+          mma_ss(tmem + (uint32_t)j.fb, ad + kk * 16u, od + kk * 16u, idesc1, acc);
+        }
+        mma_commit(smem_u32(bars + 2));
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // wait for all MMAs: the final commit's phase
+  if (t1 > t0) {
+    const int64_t ntl = t1 - t0;
+    // warp 0 consumed (ntl - 1) completions; the last one has parity (ntl - 1) & 1
+    mbar_wait(smem_u32(bars + 2), (uint32_t)((ntl - 1) & 1));
+  }
+  tc_fence_after();
+  // epilogue: thread = row m of D (lane quarter = warp), N fp32 columns
+  const int m = warp * 32 + lane;
+  float* out = j.partial + ((int64_t)blockIdx.x * 128 + m) * N;
+  for (int c = 0; c < N; c += 16) {
+    uint32_t v[32];
+    if (c + 32 <= N) {
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) out[c + i] = t1 > t0 ? __uint_as_float(v[i]) : 0.f;
+      c += 16;
+    } else {
+      uint32_t w[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+            "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]),
+            "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+          : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[c + i] = t1 > t0 ? __uint_as_float(w[i]) : 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Fixed-order reduction of the CTA partials into the gradient blob.
+//   kind 0: hidden layer l >= 2: W[m][k] <- D[m][k], b[m] <- D[m][fb]
+//   kind 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
+//   kind 2: head row `row` of the head-gradient image: v[j] <- D[row][j], c <- D[row][fb]
+struct DwReduce {
+  const float* partial;
+  int ncta, N, fb, kind, rows, m_off, row, d0, in;
+  float* w_out;  // weights (row-major [rows][in]) or head vector
+  float* b_out;
+};
+
+__global__ void k_dw_reduce(DwReduce r) {
+  const int per_row = r.in + 1;
+  const int total = r.kind == 2 ? per_row : r.rows * per_row;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int m = r.kind == 2 ? r.row : i / per_row;  // row of D
+    const int k = i % per_row;
+    float acc = 0.f;
+    for (int c = 0; c < r.ncta; ++c) {
+      const float* P = r.partial + ((int64_t)c * 128 + m) * r.N;
+      if (k == r.in) acc += P[r.fb];
+      else if (r.kind == 1) acc += P[k] + P[r.d0 + k];
+      else acc += P[k];
+    }
+    if (r.kind == 2) {
+      if (k == r.in) *r.b_out = acc;
+      else r.w_out[k] = acc;
+    } else {
+      const int mo = m + r.m_off;
+      if (k == r.in) r.b_out[mo] = acc;
+      else r.w_out[(int64_t)mo * r.in + k] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool train_tc_supported(const nb_desc& d) {
+  return d.precision == NB_BF16 && (d.width == 64 || d.width == 128) && d.hidden_layers >= 2;
+}
+
+struct TrainLayout {
+  size_t x_img, h_img[kMaxLayers], d_img[kMaxLayers], hd_img, g32, partial, total;
+};
+
+static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
+  const int W = m->d.width, L = m->d.hidden_layers;
+  const int64_t T = (n + kTile - 1) / kTile;
+  TrainLayout t;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  t.x_img = take(T * img_tile_bytes(16));
+  for (int l = 0; l < L; ++l) t.h_img[l] = take(T * img_tile_bytes(W));
+  for (int l = 0; l < L; ++l) t.d_img[l] = take(T * img_tile_bytes(W));
+  // the dW GEMM reads 128 features of A per tile: pad the last tile's images
+  take(img_tile_bytes(128));
+  t.hd_img = take(T * img_tile_bytes(8) + img_tile_bytes(128));
+  t.g32 = take((size_t)T * kTile * 3 * sizeof(float));
+  t.partial = take((size_t)grid * 128 * (kDwMaxN + 16) * sizeof(float));
+  t.total = off;
+  return t;
+}
+
+size_t train_tc_scratch_bytes(const nb_model* m, int64_t n) {
+  return train_layout(m, n, m->num_sms).total;
+}
+
+template <int W>
+static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) {
+  size_t smem = ((m->pl.bytes + 15) & ~15u) + 64;
+  smem = std::max<size_t>(smem, 116 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
+  k_bwd_tc<W><<<grid, 2 * 4 * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+static cudaError_t run_dw(nb_model* m, const DwJob& j, int64_t T, int grid, cudaStream_t st) {
+  const size_t stage = 128 * 256 + (size_t)(j.fb + 16) * 256;
+  const size_t smem = 2 * stage + 64;
+  cudaError_t e = cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_dw_tc<<<grid, 128, smem, st>>>(j, T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
+
+cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                            int64_t n_global, float alpha, float beta, cudaStream_t st) {
+  const int W = m->d.width, L = m->d.hidden_layers, d0 = m->d0;
+  const int64_t T = (n + kTile - 1) / kTile;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(T, m->num_sms));
+  TrainLayout tl = train_layout(m, n, m->num_sms);
+  uint8_t* base = (uint8_t*)m->train_scratch;
+  // 1. forward with activation images and dL/dz
+  FwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.q = q;
+  a.y = y;
+  a.n = n;
+  a.counts = m->d_counts;
+  a.keys = m->d_keys;
+  a.flags = m->d_flags;
+  a.tr.x_img = base + tl.x_img;
+  for (int l = 0; l < L; ++l) a.tr.h_img[l] = base + tl.h_img[l];
+  a.tr.hd_img = base + tl.hd_img;
+  a.tr.g32 = (float*)(base + tl.g32);
+  a.tr.alpha = alpha;
+  a.tr.beta = beta;
+  a.tr.inv_b = 1.0f / (float)n_global;
+  a.tr.loss = m->d_loss;
+  a.tr.stats = m->d_stats;
+  cudaError_t e = cudaSuccess;
+  if (n > 0) e = launch_fwd_tc(m, kTrain, a, st);
+  if (e != cudaSuccess) return e;
+  // 2. backward chain
+  BwdParams bp;
+  bp.packed = m->packed;
+  bp.pl = m->pl;
+  bp.L = L;
+  bp.nh = m->d.n_heads;
+  bp.ha0 = m->d.head_after[0];
+  bp.ha1 = m->d.head_after[1];
+  bp.n = n;
+  bp.num_tiles = T;
+  for (int l = 0; l < L; ++l) {
+    bp.h_img[l] = base + tl.h_img[l];
+    bp.d_img[l] = base + tl.d_img[l];
+  }
+  bp.g32 = (float*)(base + tl.g32);
+  if (n > 0) e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
+  if (e != cudaSuccess) return e;
+  // 3 + 4. dW GEMM jobs and their deterministic reductions
+  float* partial = (float*)(base + tl.partial);
+  auto job = [&](const uint8_t* a_img, int fa, const uint8_t* b_img, int fb, DwReduce r) {
+    DwJob j{a_img, fa, 0, b_img, fb, partial};
+    cudaError_t e2 = cudaSuccess;
+    if (n > 0) e2 = run_dw(m, j, T, grid, st);
+    else e2 = cudaMemsetAsync(partial, 0, sizeof(float) * 128 * (fb + 16) * grid, st);
+    if (e2 != cudaSuccess) return e2;
+    r.partial = partial;
+    r.ncta = grid;
+    r.N = fb + 16;
+    r.fb = fb;
+    k_dw_reduce<<<64, 256, 0, st>>>(r);
+    return cudaGetLastError();
+  };
+  float* g = m->grad;
+  for (int l = 0; l < L && e == cudaSuccess; ++l) {
+    DwReduce r{};
+    r.rows = W;
+    r.w_out = g + m->po.W[l];
+    r.b_out = g + m->po.b[l];
+    if (l == 0) {
+      r.kind = 1;
+      r.d0 = d0;
+      r.in = d0;
+      e = job(base + tl.d_img[0], W, base + tl.x_img, 16, r);
+    } else {
+      r.kind = 0;
+      r.in = W;
+      e = job(base + tl.d_img[l], W, base + tl.h_img[l - 1], W, r);
+    }
+  }
+  // output head: row 0 of the head-gradient image against h_L
+  if (e == cudaSuccess) {
+    DwReduce r{};
+    r.kind = 2;
+    r.row = 0;
+    r.in = W;
+    r.w_out = g + m->po.wout;
+    r.b_out = g + m->po.bout;
+    e = job(base + tl.hd_img, 8, base + tl.h_img[L - 1], W, r);
+  }
+  for (int k = 0; k < m->d.n_heads && e == cudaSuccess; ++k) {
+    DwReduce r{};
+    r.kind = 2;
+    r.row = 1 + k;
+    r.in = W;
+    r.w_out = g + m->po.u[k];
+    r.b_out = g + m->po.c[k];
+    e = job(base + tl.hd_img, 8, base + tl.h_img[m->d.head_after[k] - 1], W, r);
+  }
+  return e;
 }
 
 }  // namespace nb

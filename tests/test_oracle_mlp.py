@@ -282,3 +282,49 @@ def test_c1_training_reduces_fp_and_stays_conservative():
         assert c["fn"] == 0
         fp.append(c["fp"])
     assert fp[1] < fp[0]
+
+
+def test_bf16_emulated_gradient_equals_torch_straight_through():
+    """ORA_BF16_EMU gradient = the exact gradient of the bf16-precision forward
+    (R33/R34), pinned against torch autograd through an independent bf16 chain
+    whose roundings are straight-through (library routine)."""
+    a = oracle.make_arch(4, 32, 6, (2, 4))
+    th = rand_theta(a, 21, scale=1.5).astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(22)
+    q = rng.random((200, 4)).astype(np.float32)
+    y = (rng.random(200) < 0.4).astype(np.uint8)
+    loss, g, _ = oracle.loss_grad(a, th, q, y, 20.0, 1.0, mode=oracle.BF16_EMU)
+
+    def st(x, f):  # straight-through rounding
+        return x + (f(x) - x).detach()
+
+    bfr = lambda x: x.float().to(torch.bfloat16).double()   # noqa: E731
+    f32 = lambda x: x.float().double()                        # noqa: E731
+    t = torch.tensor(th, requires_grad=True)
+    x = torch.from_numpy(q)
+    hi = x.to(torch.bfloat16).float()
+    h = hi.double() + (x - hi).to(torch.bfloat16).double()
+    p, d_in, rl = 0, a.d0, {}
+    for l in range(a.layers):
+        W = t[p:p + d_in * a.width].view(a.width, d_in); p += d_in * a.width
+        b = t[p:p + a.width]; p += a.width
+        z = st(st(h @ st(W, bfr).T, f32) + b, f32)
+        r = torch.relu(z)
+        rl[l + 1] = r
+        h = st(r, bfr) if l < a.layers - 1 else r
+        d_in = a.width
+    wo = t[p:p + a.width]; p += a.width
+    bo = t[p]; p += 1
+    outs = [h @ wo + bo]
+    for k in range(a.n_heads):
+        u = t[p:p + a.width]; p += a.width
+        c = t[p]; p += 1
+        outs.append(rl[a.head_after[k]] @ u + c)  # heads read the fp32 ReLU output (R33)
+    yt = torch.from_numpy(y).double()
+    w = torch.where(yt > 0, 20.0, 1.0)
+    L = sum(torch.nn.functional.binary_cross_entropy_with_logits(st(o, f32), yt, weight=w,
+                                                                 reduction="sum") / 200 for o in outs)
+    L.backward()
+    assert loss == pytest.approx(L.item(), rel=1e-6)
+    rel = np.linalg.norm(g - t.grad.numpy()) / np.linalg.norm(t.grad.numpy())
+    assert rel < 2e-3, rel
