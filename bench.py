@@ -78,6 +78,24 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        try:  # NVML: microsecond queries, sampled every 2 ms
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = get_r(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -306,41 +324,58 @@ def run_ours(args):
 
 
 def train_rate(nb, nbgen, cfg, local, rank, world, steps):
-    """Training samples/s of the fp32 configs[0] path (bf16 training: see DESIGN.md)."""
+    """Train samples/s (BASELINE.json metric part 2) of configs[1]: one
+    nb_train_step = bf16 forward (train mode) + Eq. (1) gradient + backward +
+    dW GEMMs + (NCCL gradient allreduce) + Adam + bf16 re-pack, global batch
+    2^16 split over the ranks; batches are pre-generated and labelled on the
+    device (16 distinct fresh batches, cycled)."""
     import torch
+    import torch.distributed as dist
 
-    c1 = nbgen.CONFIGS["c1"]
-    desc = nb.Desc(c1.kind, c1.space_dim, c1.width, c1.hidden_layers, (), c1.precision)
+    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
     m = nb.Model(desc, local)
-    m.set_params(nbgen.init_params(c1))
-    g = nb.Grid(nbgen.make_grid(c1), 2, local)
-    q = nbgen.make_queries(c1, nbgen.TAG_EVAL, 0, c1.n_eval, device=f"cuda:{local}")
-    y = g.label("point", q)
-    B = c1.train_batch
+    if world > 1:
+        uid = [nb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        m.comm_init(uid[0], rank, world)
+    m.set_params(nbgen.init_params(cfg))
+    g = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
+    B = cfg.train_batch
+    b = B // world
+    dev = f"cuda:{local}"
+    qs = [nbgen.train_batch(cfg, t, rank, world, device=dev) for t in range(16)]
+    ys = [g.label(cfg.kind, q) for q in qs]
     for t in range(3):
-        m.train_step(q[:B], y[:B], alpha=1.0)
+        m.train_step(qs[t], ys[t], alpha=1.0, n_global=B)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in range(steps):
-        sl = slice((t % 16) * B, (t % 16 + 1) * B)
-        m.train_step(q[sl], y[sl], alpha=nb.alpha(t, steps))
+        m.train_step(qs[t % 16], ys[t % 16], alpha=nb.alpha(t, steps), n_global=B)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    return {"metric": "train samples/s", "value": B * steps / (ms * 1e-3), "config": "c1 fp32 2->32x2->1, batch 4096",
-            "steps": steps, "ms_per_step": ms / steps}
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item()
+    flop = 3 * flop_per_query(cfg)  # forward + delta back-propagation + dW (algorithmic)
+    return {"metric": "train samples/s", "value": B * steps / (ms * 1e-3), "unit": "samples/s",
+            "config": f"{CONFIG} bf16 3->64x4->1, global batch {B}, Adam lr 1e-3, alpha ramp",
+            "steps": steps, "ms_per_step": ms / steps,
+            "tflops_algorithmic": flop * B * steps / (ms * 1e-3) / 1e12}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
-    ap.add_argument("--train-steps", type=int, default=50)
+    ap.add_argument("--train-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
