@@ -216,9 +216,9 @@ def run_ours(args):
     desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
     m = nb.Model(desc, local)
     if world > 1:
-        uid = [nb.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        m.comm_init(uid[0], rank, world)
+        from paper_2310_06822_b200.dist import comm_init
+
+        comm_init(m)
     m.set_params(nbgen.init_params(cfg) * 2.5)
     n = N_PER_RANK
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
@@ -335,9 +335,9 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
     desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
     m = nb.Model(desc, local)
     if world > 1:
-        uid = [nb.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        m.comm_init(uid[0], rank, world)
+        from paper_2310_06822_b200.dist import comm_init
+
+        comm_init(m)
     m.set_params(nbgen.init_params(cfg))
     g = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
     B = cfg.train_batch
