@@ -24,6 +24,7 @@ SOURCES = {
     "nb_api.cu": [],
     "nb_simt.cu": [],
     "nb_fwd_tc.cu": [],
+    "nb_fwd_tc2.cu": [],
     "nb_train_tc.cu": [],
     "nb_label.cu": ["-fmad=false"],   # exact fp64 DDA rounding (no FMA contraction)
     "nb_comm.cpp": [],

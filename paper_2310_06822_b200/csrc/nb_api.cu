@@ -74,14 +74,18 @@ static void param_offsets(const nb_desc& d, int d0, ParamOffsets* o) {
 
 static uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
+// Widths above 128 run on CTA pairs (tcgen05 cta_group::2): each CTA's image
+// holds half of every layer's output rows (pl.pairs = 2 images back to back).
 static void pack_layout(const nb_desc& d, PackLayout* pl) {
   uint32_t off = 0;
   const uint32_t W = (uint32_t)d.width;
+  pl->pairs = (d.precision == NB_BF16 && W > 128) ? 2u : 1u;
+  const uint32_t rows = W / pl->pairs;
   for (int l = 0; l < d.hidden_layers; ++l) {
     const uint32_t K = l == 0 ? (uint32_t)kEncK : W;
     pl->off_w[l] = off;
     pl->k_of[l] = K;
-    off = align_up(off + W * K * 2u, 128u);
+    off = align_up(off + rows * K * 2u, 128u);
   }
   pl->off_bias = off; off = align_up(off + 4u * W * d.hidden_layers, 16u);
   pl->off_wout = off; off = align_up(off + 4u * W, 16u);
@@ -129,8 +133,9 @@ static void timing_end(const nb_model* m, cudaStream_t s) {
 static cudaError_t launch_forward_any(const nb_model* m, int mode, const FwdArgs& a,
                                       cudaStream_t s) {
   timing_begin(m, s);
-  cudaError_t e = m->d.precision == NB_BF16 ? launch_fwd_tc(m, mode, a, s)
-                                            : launch_fwd_simt(m, mode, a, s);
+  cudaError_t e = m->d.precision != NB_BF16 ? launch_fwd_simt(m, mode, a, s)
+                  : m->pl.pairs == 2        ? launch_fwd_tc2(m, mode, a, s)
+                                            : launch_fwd_tc(m, mode, a, s);
   timing_end(m, s);
   return e;
 }
@@ -208,7 +213,8 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
     set_error("invalid nb_desc");
     return NB_E_ARG;
   }
-  const bool ok_arch = desc->precision == NB_BF16 ? tc_supported(*desc) : simt_supported(*desc);
+  const bool ok_arch = desc->precision == NB_BF16 ? (tc_supported(*desc) || tc2_supported(*desc))
+                                                  : simt_supported(*desc);
   if (!ok_arch) {
     set_error("no kernel for precision %d width %d", desc->precision, desc->width);
     return NB_E_UNSUPPORTED;
@@ -234,7 +240,7 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->adam_m, sizeof(float) * m->P);
   A((void**)&m->adam_v, sizeof(float) * m->P);
   A((void**)&m->grad, sizeof(float) * m->P);
-  A((void**)&m->packed, m->pl.bytes);
+  A((void**)&m->packed, (size_t)m->pl.bytes * m->pl.pairs);
   A((void**)&m->d_tau, sizeof(float) * 4);
   A((void**)&m->d_counts, sizeof(unsigned long long) * 16);
   A((void**)&m->d_keys, sizeof(unsigned int) * 4);

@@ -1,0 +1,457 @@
+// nb_fwd_tc2.cu — fused forward + classify/count/calibrate for widths that do
+// not fit one SM (w = 256, BASELINE.json configs[4]): CTA pairs on tcgen05
+// cta_group::2 (M = 256 rows per MMA: 128 per CTA).  Same rows a1-a6 and the
+// same arithmetic as nb_fwd_tc.cu.
+//
+// Each CTA of a 2-CTA cluster holds half of every layer's weight rows in shared
+// memory (its "pair image", 196 KB for 6->256x4->1) and its own 128 rows of the
+// tile-pair in TMEM: accumulator D (256 fp32 columns) + bf16 A (128 columns).
+// The leader CTA's elected thread issues the pair's MMAs once both CTAs have
+// staged A (a_full: one cluster-scope arrive per CTA after a CTA-wide named
+// barrier) and commits them to both CTAs' acc_full barriers (multicast).
+// 16 warps per CTA: warp w reads TMEM lane quarter w % 4 and column group
+// w / 4 (64 columns); group 0 stages inputs and classifies.
+#include <cuda_bf16.h>
+
+#include "nb_device.cuh"
+#include "nb_internal.cuh"
+
+namespace nb {
+
+struct TcParams2 {
+  FwdArgs a;
+  const uint8_t* packed;  // pl.pairs images
+  PackLayout pl;
+  int d0, L, nh, ha0, ha1;
+  int64_t num_pairs;      // 256-row tile pairs
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, 10000000;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mma_ts2(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit2(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void encode_cols2(const float* x, int d0, uint32_t (&col)[8]) {
+  uint32_t h[8], l[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    __nv_bfloat16 hi = __float2bfloat16_rn(x[j]);
+    __nv_bfloat16 lo = __float2bfloat16_rn(x[j] - __bfloat162float(hi));
+    h[j] = __bfloat16_as_ushort(hi);
+    l[j] = __bfloat16_as_ushort(lo);
+  }
+  uint32_t e[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v = (k == j && j < d0) ? h[j] : v;
+      v = (k == d0 + j && j < d0) ? l[j] : v;
+    }
+    e[k] = v;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) col[c] = e[2 * c] | (e[2 * c + 1] << 16);
+}
+
+__device__ __forceinline__ void add2p(float& d0, float& d1, float a0, float a1, float b0,
+                                      float b1) {
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void fma2p(float& c0, float& c1, float a0, float a1, float b0,
+                                      float b1) {
+  asm("{.reg .b64 ra, rb, rc;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%0, %1};\n\t"
+      "fma.rn.f32x2 rc, ra, rb, rc;\n\tmov.b64 {%0, %1}, rc;}"
+      : "+f"(c0), "+f"(c1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+template <int MODE>
+__device__ __forceinline__ void classify2(uint32_t* cnt, uint32_t (&key)[3], bool valid, int y,
+                                          float z, const float* e, int nh, const float* tau,
+                                          unsigned int* flags) {
+  if (MODE == kCalibrate) {
+    if (valid && y == 1) {
+      key[0] = min(key[0], dkey(z));
+      if (nh > 0) key[1] = min(key[1], dkey(e[0]));
+      if (nh > 1) key[2] = min(key[2], dkey(e[1]));
+    }
+  }
+  if (MODE == kScore) {
+    int bin;
+    bool pred;
+    if (nh > 0 && !(e[0] >= tau[1])) { pred = false; bin = 0; }
+    else if (nh > 1 && !(e[1] >= tau[2])) { pred = false; bin = 1; }
+    else { pred = z >= tau[0]; bin = pred ? 3 : 2; }
+    const bool yy = y != 0;
+    const bool nonfin = !isfinite(z) || (nh > 0 && !isfinite(e[0])) || (nh > 1 && !isfinite(e[1]));
+    const unsigned full = 0xFFFFFFFFu;
+    const uint32_t c0 = __popc(__ballot_sync(full, valid && pred && yy));
+    const uint32_t c1 = __popc(__ballot_sync(full, valid && pred && !yy));
+    const uint32_t c2 = __popc(__ballot_sync(full, valid && !pred && yy));
+    const uint32_t c3 = __popc(__ballot_sync(full, valid && !pred && !yy));
+    const uint32_t b0 = __popc(__ballot_sync(full, valid && bin == 0));
+    const uint32_t b1 = __popc(__ballot_sync(full, valid && bin == 1));
+    const uint32_t b2 = __popc(__ballot_sync(full, valid && bin == 2));
+    const uint32_t b3 = __popc(__ballot_sync(full, valid && bin == 3));
+    const uint32_t nf = __popc(__ballot_sync(full, valid && nonfin));
+    if ((threadIdx.x & 31) == 0) {
+      cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
+      cnt[4] += b0; cnt[5] += b1; cnt[6] += b2; cnt[7] += b3; cnt[8] += nf;
+    }
+  }
+  if (valid && y > 1) atomicOr(flags, kFlagLabel);
+}
+
+template <int LC, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(const TcParams2 p) {
+  constexpr int W = 256, NWARP = 16, CPT = 64;
+  const int L = LC ? LC : p.L;
+  const int NH = p.nh;
+  const int h0 = p.nh > 0 ? p.ha0 - 1 : -1, h1 = p.nh > 1 ? p.ha1 - 1 : -1;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t rank = cluster_rank();
+  const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
+  // [0] weights  [1] acc_full  [2] a_full (leader)  [3,4] stage  [5] pad
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  float* xch = reinterpret_cast<float*>(tmem_slot + 4);                   // [2][3 groups][128][3]
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(xch + 2 * 3 * 128 * 3);      // [16][12]
+  float* qst = reinterpret_cast<float*>(ctr + NWARP * 12);                 // [2][128*8]
+  uint8_t* yst = reinterpret_cast<uint8_t*>(qst + 2 * kTile * 8);          // [2][128]
+  const uint32_t w_bar = smem_u32(bars), acc_full = smem_u32(bars + 1), a_full = smem_u32(bars + 2);
+  auto stage_bar = [&](int b) { return smem_u32(bars + 3 + b); };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(w_bar, 1);
+      mbar_init(acc_full, 1);
+      mbar_init(a_full, 2);
+      mbar_init(stage_bar(0), 1);
+      mbar_init(stage_bar(1), 1);
+      fence_barrier_init();
+      mbar_arrive_expect_tx(w_bar, p.pl.bytes);
+      const uint8_t* img = p.packed + (size_t)rank * p.pl.bytes;
+      for (uint32_t off = 0; off < p.pl.bytes; off += 32768u)
+        bulk_g2s(sbase + off, img + off, min(32768u, p.pl.bytes - off), w_bar);
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < NWARP * 12; i += blockDim.x) ctr[i] = 0u;
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  mbar_wait(w_bar, 0);
+
+  const int64_t n = p.a.n;
+  const int64_t npairs = gridDim.x / 2;
+  const int64_t pid = blockIdx.x / 2;
+  const int qw = warp & 3, grp = warp >> 2, col0 = grp * CPT;
+  const bool lead = grp == 0;
+  const bool issuer = warp == 0 && lane == 0;      // stages records, signals the leader
+  const bool leader = rank == 0;
+  const int rit = qw * 32 + lane;                  // row within this CTA's half tile
+  const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
+  const uint32_t ACOL = 256;                       // bf16 A operand columns [256, 384)
+  const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
+  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
+  const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
+  const float* cst = reinterpret_cast<const float*>(smem + p.pl.off_c);
+  const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]) + col0;
+  const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]) + col0;
+  uint32_t* cnt = ctr + warp * 12;
+  uint32_t key[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  const int nl = 1 + NH, d0 = p.d0;
+  const uint32_t idesc = make_idesc_bf16(256, W);
+  const uint32_t a_full_leader = mapa_shared(a_full, 0);
+  uint32_t ph = 0, aph = 0;
+
+  // Both CTAs staged the next A: CTA-wide named barrier, then one cluster
+  // arrive per CTA on the leader's a_full; the leader issues layer l's MMAs.
+  auto sync_and_issue = [&](int l) {
+    tc_fence_before();
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_remote(a_full_leader);
+      if (leader) {
+        while (!mbar_try_wait_cluster(a_full, aph)) {
+        }
+        aph ^= 1u;
+        tc_fence_after();
+        if (elect_one()) {
+          if (l == 0) {
+            mma_ts2(tmem, tmem + ACOL, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u),
+                    idesc, 0u);
+          } else {
+            const uint64_t bd = make_sdesc(sbase + p.pl.off_w[l], 128u, (W / 8u) * 128u);
+#pragma unroll
+            for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
+              mma_ts2(tmem, tmem + ACOL + kk * 8u, bd + (uint64_t)(kk * 16u), idesc, kk > 0u);
+          }
+          mma_commit2(acc_full);
+        }
+      }
+      __syncwarp();
+    }
+  };
+
+  auto half_base = [&](int64_t t) { return t * 2 * kTile + (int64_t)rank * kTile; };
+  auto full_half = [&](int64_t t) { return half_base(t) + kTile <= n; };
+  auto stage_issue = [&](int64_t t, int b) {
+    if (!issuer || t >= p.num_pairs || !full_half(t)) return;
+    const uint32_t qb = (uint32_t)(kTile * d0 * 4);
+    mbar_arrive_expect_tx(stage_bar(b), qb + (MODE != kForward ? (uint32_t)kTile : 0u));
+    bulk_g2s(smem_u32(qst + b * kTile * 8), p.a.q + half_base(t) * d0, qb, stage_bar(b));
+    if (MODE != kForward) bulk_g2s(smem_u32(yst + b * kTile), p.a.y + half_base(t), kTile, stage_bar(b));
+  };
+  uint32_t sph[2] = {0u, 0u};
+  int ycur = 0;
+  auto put_input = [&](int64_t t, int i) {
+    if (lead) {
+      float x[8];
+      const int b = i & 1;
+      if (full_half(t)) {
+        mbar_wait(stage_bar(b), sph[b]);
+        sph[b] ^= 1u;
+        const float* qs = qst + b * kTile * 8 + rit * d0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
+        ycur = MODE != kForward ? (int)yst[b * kTile + rit] : 0;
+      } else {
+        const int64_t r = half_base(t) + rit;
+        const bool v = r < n;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
+        ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
+      }
+      uint32_t c[8];
+      encode_cols2(x, d0, c);
+      tmem_st8(trow + ACOL, c);
+      tmem_wait_st();
+    }
+    sync_and_issue(0);
+  };
+
+  int64_t tile = pid;
+  stage_issue(tile, 0);
+  stage_issue(tile + npairs, 1);
+  int i_tile = 0;
+  if (tile < p.num_pairs) put_input(tile, 0);
+  uint32_t par = 0;
+  while (tile < p.num_pairs) {
+    const int64_t next = tile + npairs;
+    int ythis = 0;
+    float z0 = lead ? bout : 0.f, z1 = 0.f;
+    float e0a = (lead && NH > 0) ? cst[0] : 0.f, e0b = 0.f;
+    float e1a = (lead && NH > 1) ? cst[1] : 0.f, e1b = 0.f;
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : kMaxLayers); ++l) {
+      if (!LC && l >= L) break;
+      mbar_wait(acc_full, ph);
+      ph ^= 1u;
+      tc_fence_after();
+      if (l == 0) stage_issue(next + npairs, i_tile & 1);
+      const bool last = (l == L - 1);
+      const float* bias = bias_all + l * W + col0;
+      uint32_t v[CPT];
+      tmem_ld32(trow + (uint32_t)col0, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(trow + (uint32_t)col0 + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_wait_ld();
+      if (last) {
+        // the accumulator is in registers: stage the next tile-pair right away
+        ythis = ycur;
+        ++i_tile;
+        if (next < p.num_pairs) put_input(next, i_tile);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float* t = reinterpret_cast<float*>(v + 32 * c);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
+          add2p(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
+          add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
+        }
+        if (!last) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+          tmem_st16(trow + ACOL + (uint32_t)((col0 + 32 * c) / 2), pk);
+        }
+        if (l == h0 || l == h1 || last) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
+          const int o = 32 * c;
+          if (l == h0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2p(e0a, e0b, t[i], t[i + 1], u0[o + i], u0[o + i + 1]);
+          }
+          if (l == h1) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2p(e1a, e1b, t[i], t[i + 1], u1[o + i], u1[o + i + 1]);
+          }
+          if (last) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) fma2p(z0, z1, t[i], t[i + 1], wout[o + i], wout[o + i + 1]);
+          }
+        }
+      }
+      if (!last) {
+        tmem_wait_st();
+        sync_and_issue(l + 1);
+      }
+    }
+    // combine the four column groups of each row (fixed order g0 + g1 + g2 + g3)
+    float z = z0 + z1;
+    float e[2] = {e0a + e0b, e1a + e1b};
+    float* xb = xch + (size_t)par * 3 * 128 * 3;
+    if (!lead) {
+      float* o = xb + ((size_t)(grp - 1) * 128 + rit) * 3;
+      o[0] = z;
+      o[1] = e[0];
+      o[2] = e[1];
+    }
+    asm volatile("bar.sync %0, 128;" ::"r"(2 + qw) : "memory");  // the 4 warps of quarter qw
+    if (lead) {
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        const float* o = xb + ((size_t)g * 128 + rit) * 3;
+        z += o[0];
+        e[0] += o[1];
+        e[1] += o[2];
+      }
+      const int64_t r = half_base(tile) + rit;
+      const bool valid = r < n;
+      if (MODE == kForward) {
+        if (valid) {
+          p.a.logits[r * nl] = z;
+          if (NH > 0) p.a.logits[r * nl + 1] = e[0];
+          if (NH > 1) p.a.logits[r * nl + 2] = e[1];
+          if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
+          if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
+        }
+      } else {
+        classify2<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+      }
+    }
+    par ^= 1u;
+    tile = next;
+  }
+  if (lead && MODE != kForward) {
+    if (MODE == kCalibrate) {
+      for (int k = 0; k <= NH; ++k) {
+        const uint32_t mk = __reduce_min_sync(0xFFFFFFFFu, key[k]);
+        if (lane == 0 && mk != 0xFFFFFFFFu) atomicMin(p.a.keys + k, mk);
+      }
+    }
+    if (MODE == kScore && lane == 0) {
+      for (int i = 0; i < kNumCounters; ++i)
+        if (cnt[i]) atomicAdd(p.a.counts + i, (unsigned long long)cnt[i]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs (issued by the leader) and reads are done
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+bool tc2_supported(const nb_desc& d) {
+  return d.precision == NB_BF16 && d.width == 256 && d.hidden_layers >= 1 &&
+         d.hidden_layers <= kMaxLayers;
+}
+
+template <int LC, int MODE>
+static cudaError_t launch_tc2_m(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
+  TcParams2 p;
+  p.a = a;
+  p.packed = m->packed;
+  p.pl = m->pl;
+  p.d0 = m->d0;
+  p.L = m->d.hidden_layers;
+  p.nh = m->d.n_heads;
+  p.ha0 = m->d.head_after[0];
+  p.ha1 = m->d.head_after[1];
+  p.num_pairs = (a.n + 2 * kTile - 1) / (2 * kTile);
+  if (p.num_pairs == 0) return cudaSuccess;
+  const size_t smem = ((m->pl.bytes + 15) & ~15u) + 8 * 6 + 16 + sizeof(float) * 2 * 3 * 128 * 3 +
+                      4 * 16 * 12 + sizeof(float) * 2 * kTile * 8 + 2 * kTile;
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc2<LC, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int pairs = (int)std::min<int64_t>(p.num_pairs, m->num_sms / 2);
+  k_fwd_tc2<LC, MODE><<<2 * pairs, 512, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <int LC>
+static cudaError_t launch_tc2_l(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (mode == kForward) return launch_tc2_m<LC, kForward>(m, a, st);
+  if (mode == kCalibrate) return launch_tc2_m<LC, kCalibrate>(m, a, st);
+  return launch_tc2_m<LC, kScore>(m, a, st);
+}
+
+cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (mode == kTrain) return cudaErrorNotSupported;
+  if (m->d.hidden_layers == 4) return launch_tc2_l<4>(m, mode, a, st);
+  return launch_tc2_l<0>(m, mode, a, st);
+}
+
+}  // namespace nb

@@ -32,7 +32,8 @@ struct PackLayout {
   uint32_t off_bout;           // fp32 (padded to 16 B)
   uint32_t off_u[2];           // fp32 [W] per head
   uint32_t off_c;              // fp32 [2] head biases (padded)
-  uint32_t bytes;              // total, multiple of 16
+  uint32_t bytes;              // one image, multiple of 16
+  uint32_t pairs;              // 1, or 2 for CTA-pair widths (2 images, each with W/2 rows)
 };
 
 struct ParamOffsets {  // canonical fp32 blob offsets (nb.h nb_num_params)
@@ -128,7 +129,9 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s);
 cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t s);
 cudaError_t launch_fwd_simt(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
+cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 bool tc_supported(const nb_desc& d);
+bool tc2_supported(const nb_desc& d);
 bool simt_supported(const nb_desc& d);
 
 cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int64_t n,

@@ -74,9 +74,10 @@ __global__ void k_pack_bf16(PackArgs a) {
   const int W = a.W;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // CTA-pair widths: image v holds output rows [v W/2, (v+1) W/2) of each layer
+  const int rows = W / (int)a.pl.pairs;
   for (int l = 0; l < a.L; ++l) {
     const int K = (int)a.pl.k_of[l];
-    __nv_bfloat16* img = (__nv_bfloat16*)(a.out + a.pl.off_w[l]);
     for (int64_t e = tid; e < (int64_t)W * K; e += stride) {
       int n = (int)(e / K), k = (int)(e % K);
       float v;
@@ -86,7 +87,10 @@ __global__ void k_pack_bf16(PackArgs a) {
       } else {
         v = a.theta[a.po.W[l] + (int64_t)n * W + k];
       }
-      int64_t off = (int64_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8);
+      const int img_i = n / rows, nl = n % rows;
+      __nv_bfloat16* img =
+          (__nv_bfloat16*)(a.out + (size_t)img_i * a.pl.bytes + a.pl.off_w[l]);
+      int64_t off = (int64_t)(nl / 8) * (K / 8) * 64 + (k / 8) * 64 + (nl % 8) * 8 + (k % 8);
       img[off] = __float2bfloat16_rn(v);
     }
   }
@@ -121,7 +125,13 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s) {
   a.d0 = m->d0;
   a.nh = m->d.n_heads;
   k_pack_bf16<<<148, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  // CTA-pair images: replicate the fp32 tail (biases, output, heads) of image 0
+  for (uint32_t i = 1; i < m->pl.pairs && e == cudaSuccess; ++i)
+    e = cudaMemcpyAsync(m->packed + (size_t)i * m->pl.bytes + m->pl.off_bias,
+                        m->packed + m->pl.off_bias, m->pl.bytes - m->pl.off_bias,
+                        cudaMemcpyDeviceToDevice, s);
+  return e;
 }
 
 // ---------------------------------------------------------------------------

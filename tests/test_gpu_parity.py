@@ -58,8 +58,6 @@ def test_labeller_ray_edge_cases():
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_encode_bit_exact(name):
     cfg = nbgen.CONFIGS[name]
-    if cfg.width > 128:
-        pytest.skip("w=256 kernel not built yet")
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 5000)
     m = nb.Model(desc_of(cfg), DEV)
     x = m.encode(cuda(q)).cpu().numpy().view(np.uint16)
@@ -148,7 +146,8 @@ def test_c1_training_run_conservative():
 
 
 # ---------------------------------------------------------------- bf16 tensor-core path
-BF16_CASES = [("c2", (1 << 16) + 77), ("c3", (1 << 15) + 5), ("c4", (1 << 15) + 129)]
+BF16_CASES = [("c2", (1 << 16) + 77), ("c3", (1 << 15) + 5), ("c4", (1 << 15) + 129),
+              ("c5", (1 << 15) + 200)]
 
 
 @pytest.mark.parametrize("name,n", BF16_CASES)
