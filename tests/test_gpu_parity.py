@@ -314,3 +314,44 @@ def test_bf16_training_run_conservative():
     m.calibrate(qe, ye)
     c = m.score(qe, ye)
     assert c["fn"] == 0 and c["fp"] < fp0, (c, fp0)
+
+
+# ---------------------------------------------------------------- full BASELINE.json sizes
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_full_size_sampled_parity(name):
+    """At the config's full N (c2 2^22, c3 2^24, c4 2^26, c5 2^28) in the launch
+    configuration bench.py uses: properties that hold at any size (FN = 0 after
+    calibration, count identities, fused score == forward + threshold) plus
+    sampled rows checked one by one against the oracle (labels bit-exact,
+    sigmoid within 2e-2 of fp64, logit vs bf16-precision oracle)."""
+    cfg = nbgen.CONFIGS[name]
+    N = cfg.n_eval
+    dev = f"cuda:{DEV}"
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, N, device=dev)
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), cfg.space_dim, DEV)
+    y = g.label(cfg.kind, q)
+    th = scaled_params(cfg, 10)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    tau = m.calibrate(q, y).numpy()
+    c = m.score(q, y)
+    npos = int(y.sum().item())
+    assert c["fn"] == 0
+    assert c["tp"] == npos and c["tp"] + c["fp"] + c["fn"] + c["tn"] == N
+    assert sum(c["exit_hist"]) == N and c["nonfinite"] == 0
+    z = m.forward(q)
+    zt = torch.tensor(tau, device=dev)
+    pred = (z >= zt).all(dim=1)
+    assert int((pred & (y == 0)).sum().item()) == c["fp"]
+    # sampled rows, one by one against the oracle
+    rng = np.random.default_rng(11)
+    idx = np.sort(rng.choice(N, 3000, replace=False))
+    it = torch.from_numpy(idx).to(dev)
+    qs = q[it].cpu().numpy()
+    assert np.array_equal(y[it].cpu().numpy(), labels_oracle(cfg, qs))
+    zs = z[it].cpu().double().numpy()
+    a = oracle.arch_of(cfg)
+    zr = oracle.forward(a, th.double().numpy(), qs)
+    assert np.abs(sigmoid(zs) - sigmoid(zr)).max() <= 2e-2
+    ze = oracle.forward(a, th.double().numpy(), qs, oracle.BF16_EMU)
+    assert (np.abs(zs - ze) < BAND).mean() > 0.99
