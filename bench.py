@@ -7,7 +7,8 @@ with the calibrated threshold -> FP/FN/TP/TN counts -> NCCL allreduce of the
 counts across ranks) over one batch of BASELINE.json configs[1] ("c2": 3D
 point bounding, 3 -> 64x4 -> 1 bf16, 2^22 uniform points per forward pass).
 Inputs are seeded synthetic (nbgen), labels come from the library's GPU
-labeller, thresholds from nb_calibrate; the timed region is nb_score only.
+labeller, thresholds from nb_calibrate; the timed region is nb_score_async
+(kernel + count allreduce + the step's count readback into pinned memory).
 
 Weak scaling: every rank scores its own 2^22-query shard (rows r*2^22.. of the
 EVAL stream); value = all ranks' queries / max-over-ranks device time.
@@ -228,11 +229,19 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        return m.score(q, y)
+    # one step = nb_score_async: fused encode/MLP/classify/count kernel, NCCL
+    # allreduce of the counts (N > 1), async copy of the step's counts into its
+    # own pinned host row; the host synchronises once after the timed loop.
+    out = torch.zeros(max(args.steps, args.warmup), 9, dtype=torch.int64).pin_memory()
 
-    for _ in range(args.warmup):
-        c = step()
+    def step(i):
+        m.score_async(q, y, out[i])
+
+    c = m.score(q, y)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    assert all(m.counts_dict(out[i]) == c for i in range(args.warmup)), (c, out)
     assert c["fn"] == 0, c
     # ---------------- timed region (device time, per-step events) ----------------
     m.set_timing(True)
@@ -246,9 +255,10 @@ def run_ours(args):
         for i in range(args.steps):
             flush.fill_(i & 0xFF)                 # evict the inputs from L2 (untimed)
             evs[i][0].record(stream)
-            c = step()
+            step(i)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
+    assert all(m.counts_dict(out[i]) == c for i in range(args.steps)), "per-step counts differ"
     if world > 1:
         dist.barrier()
     kernel_ms, launches = m.kernel_time()

@@ -170,6 +170,14 @@ nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n,
  * yhat = [e_1 >= tau_1] and [e_2 >= tau_2] and [z >= tau]; counts to *out (host). */
 nb_status nb_score(const nb_model* m, const float* q, const uint8_t* y, int64_t n,
                    nb_counts* out, void* stream);
+/* Asynchronous nb_score: the same kernel, allreduce and counts, but the counts
+ * are copied (cudaMemcpyAsync, cudaMemcpyDefault) to `out`, which must be
+ * pinned host or device memory, when `stream` gets there; nothing synchronises.
+ * Sticky in-kernel flags are reported by the next synchronising call.  The
+ * model's counter scratch is reused, so calls on one model must be issued on
+ * one stream (they serialise there).                                       */
+nb_status nb_score_async(const nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                         nb_counts* out, void* stream);
 /* Same as nb_score with HOST q/y (pinned or pageable): the library streams the
  * records to the device in chunks, overlapping copies with the fused kernel
  * (end-to-end serving path).                                              */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "nb_calibrate": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score_host": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_score_async": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
     "nb_alpha": (_D, [_I64, _I64]),
     "nb_grid_create": (C.c_int, [_I32, _I32, _I32, _P, _I32, _P]),
@@ -293,6 +294,22 @@ class Model:
         _check(lib().nb_score(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
                               q.shape[0], C.byref(c), _stream(self.device)), "nb_score")
         return c.as_dict()
+
+    def score_async(self, q: torch.Tensor, y: torch.Tensor, out: torch.Tensor) -> None:
+        """nb_score_async: counts land in `out` (uint64/int64 [9], pinned host or
+        on this device) when the current stream gets there; no synchronisation."""
+        if out.dtype not in (torch.int64, torch.uint64) or out.numel() != 9 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous 9-element 64-bit tensor")
+        if out.device.type == "cpu" and not out.is_pinned():
+            raise ValueError("host out must be pinned")
+        _check(lib().nb_score_async(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
+                                    q.shape[0], out.data_ptr(), _stream(self.device)),
+               "nb_score_async")
+
+    @staticmethod
+    def counts_dict(out: torch.Tensor) -> dict:
+        v = [int(x) for x in out.cpu().view(torch.int64).tolist()]
+        return dict(tp=v[0], fp=v[1], fn=v[2], tn=v[3], exit_hist=v[4:8], nonfinite=v[8])
 
     def score_host(self, q: torch.Tensor, y: torch.Tensor) -> dict:
         if q.device.type != "cpu" or y.device.type != "cpu":

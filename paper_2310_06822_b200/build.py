@@ -24,12 +24,18 @@ SOURCES = {
     "nb_api.cu": [],
     "nb_simt.cu": [],
     "nb_fwd_tc.cu": [],
+    "nb_fwd_tc_w64l4_d3.cu": [],
+    "nb_fwd_tc_w128l4_d6.cu": [],
+    "nb_fwd_tc_w128l6h24_d4.cu": [],
+    "nb_fwd_tc_gen32.cu": [],
+    "nb_fwd_tc_gen64.cu": [],
+    "nb_fwd_tc_gen128.cu": [],
     "nb_fwd_tc2.cu": [],
     "nb_train_tc.cu": [],
     "nb_label.cu": ["-fmad=false"],   # exact fp64 DDA rounding (no FMA contraction)
     "nb_comm.cpp": [],
 }
-HEADERS = ["nb_internal.cuh", "nb_device.cuh"]
+HEADERS = ["nb_internal.cuh", "nb_device.cuh", "nb_fwd_tc.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

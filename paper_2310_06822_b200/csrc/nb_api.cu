@@ -95,6 +95,18 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
     if (k < d.n_heads) off = align_up(off + 4u * W, 16u);
   }
   pl->off_c = off; off += 16u;
+  off = align_up(off, 128u);
+  pl->core_bytes = off;
+  const bool fold = pl->pairs == 1 && d.precision == NB_BF16;
+  const int d0 = (int)nb_record_floats(d.kind, d.space_dim);
+  pl->bias_l0 = (fold && 2 * d0 + 3 <= kEncK) ? 1u : 0u;
+  for (int l = 0; l < kMaxLayers; ++l) {
+    pl->off_bb[l] = 0;
+    if (fold && l >= 1 && l < d.hidden_layers) {
+      pl->off_bb[l] = off;
+      off = align_up(off + W * (uint32_t)kEncK * 2u, 128u);
+    }
+  }
   pl->bytes = align_up(off, 16u);
 }
 
@@ -487,6 +499,21 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
   NB_CUDA(cudaStreamSynchronize(s));
   counts_out(hc, out);
   return take_flags(m, s, NB_OK);
+}
+
+nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, int64_t n,
+                         nb_counts* out, void* stream) {
+  static_assert(sizeof(nb_counts) == sizeof(unsigned long long) * kNumCounters, "nb_counts layout");
+  nb_model* m = const_cast<nb_model*>(m_);
+  if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
+  if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
+  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
+  // the device counter order is the nb_counts field order (tp fp fn tn exit[4] nonfinite)
+  NB_CUDA(cudaMemcpyAsync(out, m->d_counts, sizeof(nb_counts), cudaMemcpyDefault, s));
+  return NB_OK;
 }
 
 nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, int64_t n,

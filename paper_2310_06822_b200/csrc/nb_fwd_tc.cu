@@ -1,518 +1,8 @@
-// nb_fwd_tc.cu — fused MLP forward + classify/count/calibrate on tcgen05
-// tensor cores (sm_100a).  Hot-path rows a1-a6:
-//   a1 encode (fp32 record -> bf16 hi/lo pair, in the epilogue warps),
-//   a2/a3 layers z_l = W_l h_{l-1} + b_l on tcgen05.mma (M=128 rows per tile,
-//         N = w, K = 16 or w; A = activations in TMEM, B = weights in SMEM),
-//         epilogue bias + ReLU + RNE bf16 pack back into TMEM as the next A,
-//   a4 output / exit-head dot products in fp32 on the epilogue threads,
-//   a5/a6 classify with the calibrated thresholds and count (warp ballots),
-//         or fold the positives' logits into the calibration minimum.
-// Paper: MLP P:285-290 §3.4, early-out heads P:258-277 §3.3, cost cases
-// P:157-176 §3.1.  Activations never leave the SM (TMEM is the tensor core's
-// register file); weights are bulk-copied into shared memory once per CTA.
-//
-// CTA (persistent, one per SM) = NSLOT x WPS epilogue warps + 1 MMA warp.
-// Each slot owns one 128-row tile in flight; its WPS warps split the tile's
-// columns (warp w reads TMEM lane quarter w % 4, column half (w % WPS) / 4).
-// The MMA thread walks the slots round-robin layer by layer, so one slot's
-// epilogue overlaps the other slots' MMAs.  Synchronisation: mbarriers
-// a_full[s] (epilogue -> MMA: next A operand is in TMEM) and acc_full[s]
-// (tcgen05.commit -> epilogue: accumulator ready).
-// Measured primitive costs that shape this plan (tools/tmem_bench.cu): an
-// M=128 K=16 MMA costs >= 46 cycles for N <= 64 and N/2 cycles for N >= 128;
-// one warp's tcgen05.ld of 64 columns + wait costs ~93 cycles, so the
-// epilogue needs many warps and all loads of a layer issued before one wait.
-#include <cuda_bf16.h>
-
-#include "nb_device.cuh"
-#include "nb_internal.cuh"
+// nb_fwd_tc.cu — dispatcher of the fused tcgen05 forward kernels
+// (nb_fwd_tc.cuh) and the generic instantiations (run-time d0, L, heads).
+#include "nb_fwd_tc.cuh"
 
 namespace nb {
-
-struct TcParams {
-  FwdArgs a;
-  const uint8_t* packed;
-  PackLayout pl;
-  int d0, L, nh, ha0, ha1;
-  int64_t num_tiles;
-  unsigned long long* trace;  // NB_TRACE builds only: timeline of CTA 0
-};
-
-#ifdef NB_TRACE
-// Debug timeline (tools/trace_fwd.py): each tracing thread of CTA 0 owns a
-// region of 2000 (clock64, code) pairs; stores only, no atomics on the path.
-#define NB_TR(region, code)                                                          \
-  do {                                                                               \
-    if (blockIdx.x == 0 && p.trace && tr_i < 2000) {                                 \
-      p.trace[((region) * 2000 + tr_i) * 2] = clock64();                            \
-      p.trace[((region) * 2000 + tr_i) * 2 + 1] = (unsigned long long)(code);       \
-      ++tr_i;                                                                        \
-    }                                                                                \
-  } while (0)
-#else
-#define NB_TR(region, code) \
-  do {                      \
-  } while (0)
-#endif
-#define NB_EV(type, s, l) ((type) | ((s) << 4) | ((l) << 8))
-
-__device__ __forceinline__ void encode_cols(const float* x, int d0, uint32_t (&col)[8]) {
-  uint32_t h[8], l[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    __nv_bfloat16 hi = __float2bfloat16_rn(x[j]);
-    __nv_bfloat16 lo = __float2bfloat16_rn(x[j] - __bfloat162float(hi));
-    h[j] = __bfloat16_as_ushort(hi);
-    l[j] = __bfloat16_as_ushort(lo);
-  }
-  // element e of the 16-wide row: e < d0 -> hi[e]; d0 <= e < 2 d0 -> lo[e - d0]; else 0
-  uint32_t e[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      v = (k == j && j < d0) ? h[j] : v;
-      v = (k == d0 + j && j < d0) ? l[j] : v;
-    }
-    e[k] = v;
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) col[c] = e[2 * c] | (e[2 * c + 1] << 16);
-}
-
-__device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
-  asm("{.reg .b64 ra, rb, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-__device__ __forceinline__ void fma2(float& c0, float& c1, float a0, float a1, float b0, float b1) {
-  asm("{.reg .b64 ra, rb, rc;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%0, %1};\n\t"
-      "fma.rn.f32x2 rc, ra, rb, rc;\n\tmov.b64 {%0, %1}, rc;}"
-      : "+f"(c0), "+f"(c1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-
-// Classification with per-warp counters kept in shared memory (lane 0 adds
-// the warp's ballot counts) to save registers in the epilogue warps.
-template <int MODE>
-__device__ __forceinline__ void classify_row_smem(uint32_t* cnt, uint32_t (&key)[3], bool valid,
-                                                  int y, float z, const float* e, int nh,
-                                                  const float* tau, unsigned int* flags) {
-  if (MODE == kCalibrate) {
-    if (valid && y == 1) {
-      key[0] = min(key[0], dkey(z));
-      if (nh > 0) key[1] = min(key[1], dkey(e[0]));
-      if (nh > 1) key[2] = min(key[2], dkey(e[1]));
-    }
-  }
-  if (MODE == kScore) {
-    int bin;
-    bool pred;
-    if (nh > 0 && !(e[0] >= tau[1])) { pred = false; bin = 0; }
-    else if (nh > 1 && !(e[1] >= tau[2])) { pred = false; bin = 1; }
-    else { pred = z >= tau[0]; bin = pred ? 3 : 2; }
-    const bool yy = y != 0;
-    const bool nonfin = !isfinite(z) || (nh > 0 && !isfinite(e[0])) || (nh > 1 && !isfinite(e[1]));
-    const unsigned full = 0xFFFFFFFFu;
-    const uint32_t c0 = __popc(__ballot_sync(full, valid && pred && yy));
-    const uint32_t c1 = __popc(__ballot_sync(full, valid && pred && !yy));
-    const uint32_t c2 = __popc(__ballot_sync(full, valid && !pred && yy));
-    const uint32_t c3 = __popc(__ballot_sync(full, valid && !pred && !yy));
-    const uint32_t b0 = __popc(__ballot_sync(full, valid && bin == 0));
-    const uint32_t b1 = __popc(__ballot_sync(full, valid && bin == 1));
-    const uint32_t b2 = __popc(__ballot_sync(full, valid && bin == 2));
-    const uint32_t b3 = __popc(__ballot_sync(full, valid && bin == 3));
-    const uint32_t nf = __popc(__ballot_sync(full, valid && nonfin));
-    if ((threadIdx.x & 31) == 0) {
-      cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
-      cnt[4] += b0; cnt[5] += b1; cnt[6] += b2; cnt[7] += b3; cnt[8] += nf;
-    }
-  }
-  if (valid && y > 1) atomicOr(flags, kFlagLabel);
-}
-
-template <int MODE>
-__device__ __forceinline__ void flush_smem(const uint32_t* cnt, uint32_t (&key)[3], int nh,
-                                           unsigned long long* counts, unsigned int* keys) {
-  const int lane = threadIdx.x & 31;
-  if (MODE == kCalibrate) {
-    for (int k = 0; k <= nh; ++k) {
-      const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, key[k]);
-      if (lane == 0 && m != 0xFFFFFFFFu) atomicMin(keys + k, m);
-    }
-  }
-  if (MODE == kScore && lane == 0) {
-    for (int i = 0; i < kNumCounters; ++i)
-      if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
-  }
-}
-
-template <int W>
-struct TcPlan;
-template <>
-struct TcPlan<32> { static constexpr int NSLOT = 4, WPS = 4, COLS = 256; };
-template <>
-struct TcPlan<64> { static constexpr int NSLOT = 5, WPS = 4, COLS = 512; };
-template <>
-struct TcPlan<128> { static constexpr int NSLOT = 2, WPS = 8, COLS = 512; };
-
-// LC / H0C / H1C: compile-time layer count and exit-head layers (1-based, 0 =
-// none) of the specialised instantiations; LC == 0 selects the generic kernel
-// that reads them from TcParams at run time.
-//
-// There is no dedicated MMA warp: each slot's lead warp (lane quarter 0,
-// column half 0) issues its own slot's MMAs right after the slot's warps
-// meet at a named barrier, so every slot is an independent chain
-//   [stage A in TMEM] -> bar.sync -> MMA layer l -> commit -> acc_full ->
-//   [epilogue l: ld, bias, ReLU, bf16 pack, st] -> bar.sync -> MMA layer l+1
-// and the tensor pipe interleaves the slots' MMAs (no head-of-line blocking).
-template <int W, int LC, int H0C, int H1C, int MODE>
-__global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
-    k_fwd_tc(const TcParams p) {
-  const int L = LC ? LC : p.L;
-  const int NH = LC ? ((H0C ? 1 : 0) + (H1C ? 1 : 0)) : p.nh;
-  const int h0 = LC ? H0C - 1 : (p.nh > 0 ? p.ha0 - 1 : -1);
-  const int h1 = LC ? H1C - 1 : (p.nh > 1 ? p.ha1 - 1 : -1);
-  constexpr int NSLOT = TcPlan<W>::NSLOT, WPS = TcPlan<W>::WPS, COLS = TcPlan<W>::COLS;
-  constexpr int NEPI = NSLOT * WPS;        // warps
-  constexpr int CPT = W * 4 / WPS;         // accumulator columns per thread
-  constexpr int NCH = CPT / 32;            // 32-column chunks per thread
-  // With enough registers all of a layer's loads are issued before one wait,
-  // and the next tile is staged as soon as the last layer's accumulator is in
-  // registers (its layer-0 MMA then overlaps this tile's output epilogue).
-  constexpr bool kAllLoads = NEPI <= 16;
-  static_assert(CPT % 32 == 0, "chunking");
-  static_assert(NSLOT * W + NSLOT * (W / 2) <= COLS, "TMEM plan");
-  static_assert(NSLOT <= 7, "named barriers 1..NSLOT and 8..");
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
-  // bars[0] weights, bars[1 + s] acc_full of slot s
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * NSLOT);  // 16-B aligned
-  float* xch = reinterpret_cast<float*>(tmem_slot + 4);  // [NSLOT][2][4][32][3] head partials
-  uint32_t* ctr = reinterpret_cast<uint32_t*>(xch + NSLOT * 2 * 4 * 32 * 3);  // [NEPI][12]
-  uint64_t* sbars = reinterpret_cast<uint64_t*>(ctr + NEPI * 12);            // [NSLOT][2]
-  float* qst = reinterpret_cast<float*>(sbars + 2 * NSLOT);                  // [NSLOT][2][128*8]
-  uint8_t* yst = reinterpret_cast<uint8_t*>(qst + NSLOT * 2 * kTile * 8);   // [NSLOT][2][128]
-  auto stage_bar = [&](int s, int b) { return smem_u32(sbars + 2 * s + b); };
-  auto q_stage = [&](int s, int b) { return qst + (size_t)(2 * s + b) * kTile * 8; };
-  auto y_stage = [&](int s, int b) { return yst + (size_t)(2 * s + b) * kTile; };
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef NB_TRACE
-  unsigned long long tr_i = 0;
-#endif
-  auto acc_full = [&](int s) { return smem_u32(bars + 1 + s); };
-  auto acc_col = [](int s) { return (uint32_t)(s * W); };
-  auto a_col = [](int s) { return (uint32_t)(NSLOT * W + s * (W / 2)); };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint32_t w_bar = smem_u32(bars);
-      mbar_init(w_bar, 1);
-      for (int s = 0; s < NSLOT; ++s) {
-        mbar_init(acc_full(s), 1);
-        mbar_init(stage_bar(s, 0), 1);
-        mbar_init(stage_bar(s, 1), 1);
-      }
-      fence_barrier_init();
-      mbar_arrive_expect_tx(w_bar, p.pl.bytes);
-      for (uint32_t off = 0; off < p.pl.bytes; off += 32768u) {
-        const uint32_t len = min(32768u, p.pl.bytes - off);
-        bulk_g2s(sbase + off, p.packed + off, len, w_bar);
-      }
-    }
-    __syncwarp();
-    tmem_alloc<COLS>(smem_u32(tmem_slot));
-  }
-  for (int i = threadIdx.x; i < NEPI * 12; i += blockDim.x) ctr[i] = 0u;
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  mbar_wait(smem_u32(bars), 0);
-
-  const int64_t n = p.a.n;
-  const int64_t G = gridDim.x;
-
-  const int s = warp / WPS;              // tile slot
-  const int qw = warp & 3;               // TMEM lane quarter
-  const int half = (warp % WPS) >> 2;    // column half (WPS == 8)
-  const int col0 = half * CPT;
-  const bool lead = half == 0;           // owns input staging and classification
-  const bool mma_warp = (warp % WPS) == 0;             // issues the slot's MMAs
-  const bool issuer = mma_warp && lane == 0;           // stages the slot's records
-  const int rit = qw * 32 + lane;        // row within the tile
-  const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
-  const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
-  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
-  const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
-  const float* cst = reinterpret_cast<const float*>(smem + p.pl.off_c);
-  const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]) + col0;
-  const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]) + col0;
-  uint32_t* cnt = ctr + warp * 12;       // per-warp counters in shared memory
-  uint32_t key[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-  uint32_t ph = 0;
-  const int nl = 1 + NH;
-  const uint32_t slot_bar = 1u + (uint32_t)s;              // all WPS warps of the slot
-  const uint32_t half_bar = 8u + (uint32_t)(s * 4 + qw);   // the 2 warps of a row quarter
-  const int d0 = p.d0;
-  const uint32_t idesc = make_idesc_bf16(128, W);
-
-  // all warps of the slot have stored the next A operand: the lead warp issues
-  // layer l's MMAs (one elected lane) and commits them to acc_full[s]
-  auto sync_and_issue = [&](int l) {
-    tc_fence_before();
-    asm volatile("bar.sync %0, %1;" ::"r"(slot_bar), "n"(WPS * 32) : "memory");
-    if (mma_warp) {
-      if (lane == 0) NB_TR(1 + s, NB_EV(0, s, l));
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t d = tmem + acc_col(s);
-        const uint32_t a = tmem + a_col(s);
-        if (l == 0) {
-          mma_ts(d, a, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u), idesc, 0u);
-        } else {
-          const uint64_t bdesc = make_sdesc(sbase + p.pl.off_w[l], 128u, (W / 8u) * 128u);
-#pragma unroll
-          for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
-            mma_ts(d, a + kk * 8u, bdesc + (uint64_t)(kk * 16u), idesc, kk > 0u);
-        }
-        mma_commit(acc_full(s));
-      }
-      __syncwarp();
-      if (lane == 0) NB_TR(1 + s, NB_EV(1, s, l));
-    }
-  };
-
-  // Records of a full tile are staged into shared memory by the TMA bulk-copy
-  // engine one tile ahead (double-buffered per slot); a ragged last tile is
-  // read directly.
-  auto full_tile = [&](int64_t t) { return (t + 1) * kTile <= n; };
-  auto stage_issue = [&](int64_t t, int b) {
-    if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
-    const uint32_t qb = (uint32_t)(kTile * d0 * 4);
-    const uint32_t bar = stage_bar(s, b);
-    mbar_arrive_expect_tx(bar, qb + (MODE != kForward ? (uint32_t)kTile : 0u));
-    bulk_g2s(smem_u32(q_stage(s, b)), p.a.q + t * kTile * d0, qb, bar);
-    if (MODE != kForward) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
-  };
-  uint32_t sph[2] = {0u, 0u};
-  int ycur = 0;
-  // encode the slot's i-th tile t into the slot's TMEM A region, then issue layer 0
-  auto put_input = [&](int64_t t, int i) {
-    if (lead) {
-      float x[8];
-      const int b = i & 1;
-      if (full_tile(t)) {
-        mbar_wait(stage_bar(s, b), sph[b]);
-        sph[b] ^= 1u;
-        const float* qs = q_stage(s, b) + rit * d0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
-        ycur = MODE != kForward ? (int)y_stage(s, b)[rit] : 0;
-      } else {
-        const int64_t r = t * kTile + rit;
-        const bool v = r < n;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
-        ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
-      }
-      uint32_t c[8];
-      encode_cols(x, d0, c);
-      tmem_st8(trow + a_col(s), c);
-      if (MODE == kTrain) {  // layer-1 input image for the dW GEMM
-        uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(16);
-#pragma unroll
-        for (int fg = 0; fg < 2; ++fg)
-          *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
-              make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
-      }
-      tmem_wait_st();
-    }
-    if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(5, s, 0));
-    sync_and_issue(0);
-  };
-
-  int64_t tile = blockIdx.x + (int64_t)s * G;
-  stage_issue(tile, 0);
-  stage_issue(tile + NSLOT * G, 1);
-  int i_tile = 0;
-  if (tile < p.num_tiles) put_input(tile, 0);
-  uint32_t par = 0;
-  while (tile < p.num_tiles) {
-    const int64_t next = tile + NSLOT * G;
-    int ythis = 0;
-    float z0 = lead ? bout : 0.f, z1 = 0.f;
-    float e0a = (lead && NH > 0) ? cst[0] : 0.f, e0b = 0.f;
-    float e1a = (lead && NH > 1) ? cst[1] : 0.f, e1b = 0.f;
-#pragma unroll
-    for (int l = 0; l < (LC ? LC : kMaxLayers); ++l) {
-      if (!LC && l >= L) break;
-      mbar_wait(acc_full(s), ph);
-      if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(2, s, l));
-      ph ^= 1u;
-      tc_fence_after();
-      // layer 0 of this tile has consumed its staged input: refill that buffer
-      if (l == 0) stage_issue(next + NSLOT * G, i_tile & 1);
-      const bool last = (l == L - 1);
-      const float* bias = bias_all + l * W + col0;
-      uint32_t v[kAllLoads ? CPT : 32];
-      if (kAllLoads) {
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-          tmem_ld32(trow + acc_col(s) + (uint32_t)(col0 + 32 * c),
-                    *reinterpret_cast<uint32_t(*)[32]>(v + (kAllLoads ? 32 * c : 0)));
-        tmem_wait_ld();
-      }
-      if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(3, s, l));
-      if (kAllLoads && last) {
-        // the accumulator is in registers and the last MMA has completed: stage
-        // the slot's next tile now so its layer-0 MMA overlaps this epilogue
-        ythis = ycur;
-        ++i_tile;
-        if (next < p.num_tiles) put_input(next, i_tile);
-      }
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (!kAllLoads) {
-          tmem_ld32(trow + acc_col(s) + (uint32_t)(col0 + 32 * c),
-                    *reinterpret_cast<uint32_t(*)[32]>(v));
-          tmem_wait_ld();
-        }
-        float* t = reinterpret_cast<float*>(v + (kAllLoads ? 32 * c : 0));
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
-          add2(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
-          add2(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
-        }
-        if (!last || MODE == kTrain) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
-          if (!last) tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
-          if (MODE == kTrain) {  // h_{l+1} image (activations kept for back-propagation)
-            uint8_t* base = p.a.tr.h_img[l] + tile * img_tile_bytes(W);
-            const int fg0 = (col0 + 32 * c) / 8;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              *reinterpret_cast<uint4*>(base + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
-                  make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-          }
-        }
-        if (l == h0 || l == h1 || last) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
-          const int o = 32 * c;
-          if (l == h0) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(e0a, e0b, t[i], t[i + 1], u0[o + i], u0[o + i + 1]);
-          }
-          if (l == h1) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(e1a, e1b, t[i], t[i + 1], u1[o + i], u1[o + i + 1]);
-          }
-          if (last) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(z0, z1, t[i], t[i + 1], wout[o + i], wout[o + i + 1]);
-          }
-        }
-      }
-      if (!last) {
-        tmem_wait_st();
-        if (mma_warp && lane == 0) NB_TR(1 + s, NB_EV(4, s, l));
-        sync_and_issue(l + 1);
-      }
-    }
-    if (!kAllLoads) {
-      ythis = ycur;
-      ++i_tile;
-      if (next < p.num_tiles) put_input(next, i_tile);
-    }
-    float z = z0 + z1;
-    float e[2] = {e0a + e0b, e1a + e1b};
-    if (WPS == 8) {  // combine the two column halves of each row
-      float* xb = xch + ((((size_t)s * 2 + par) * 4 + qw) * 32 + lane) * 3;
-      if (!lead) {
-        xb[0] = z;
-        xb[1] = e[0];
-        xb[2] = e[1];
-      }
-      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "n"(64) : "memory");
-      if (lead) {
-        z += xb[0];
-        e[0] += xb[1];
-        e[1] += xb[2];
-      }
-      par ^= 1u;
-    }
-    if (lead) {
-      const int64_t r = tile * kTile + rit;
-      const bool valid = r < n;
-      if (MODE == kForward) {
-        if (valid) {
-          p.a.logits[r * nl] = z;
-          if (NH > 0) p.a.logits[r * nl + 1] = e[0];
-          if (NH > 1) p.a.logits[r * nl + 2] = e[1];
-          if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
-          if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
-        }
-      } else if (MODE == kTrain) {
-        // Eq. (1): w = alpha if y else beta; term w softplus(-+z);
-        // dL/dz = w (sigmoid(z) - y) / B; exit heads add the same term
-        const float yf = (float)ythis;
-        const float w = valid ? (ythis ? p.a.tr.alpha : p.a.tr.beta) : 0.f;
-        auto sp = [](float u) { return fmaxf(u, 0.f) + log1pf(__expf(-fabsf(u))); };
-        float lsum = w * sp(ythis ? -z : z);
-        const float gz = w * (1.f / (1.f + __expf(-z)) - yf) * p.a.tr.inv_b;
-        float ge[2] = {0.f, 0.f};
-        for (int k = 0; k < NH; ++k) {
-          lsum += w * sp(ythis ? -e[k] : e[k]);
-          ge[k] = w * (1.f / (1.f + __expf(-e[k])) - yf) * p.a.tr.inv_b;
-        }
-        const int64_t r3 = r * 3;
-        if (valid) {
-          p.a.tr.g32[r3] = gz;
-          p.a.tr.g32[r3 + 1] = ge[0];
-          p.a.tr.g32[r3 + 2] = ge[1];
-        }
-        uint8_t* hb = p.a.tr.hd_img + tile * img_tile_bytes(8) + (rit / 8) * 128 + (rit % 8) * 16;
-        *reinterpret_cast<uint4*>(hb) = make_uint4(pack_bf16x2(gz, ge[0]), pack_bf16x2(ge[1], 0.f), 0u, 0u);
-        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xFFFFFFFFu, lsum, o);
-        const bool pred = z >= 0.f, yy = ythis != 0;
-        const uint32_t c0 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
-        const uint32_t c1 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
-        const uint32_t c2 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && yy));
-        const uint32_t c3 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
-        if (lane == 0) {
-          atomicAdd(p.a.tr.loss, (double)lsum * (double)p.a.tr.inv_b);
-          cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
-        }
-      } else {
-        classify_row_smem<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
-      }
-    }
-    tile = next;
-  }
-  if ((MODE == kCalibrate || MODE == kScore) && lead)
-    flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
-  if (MODE == kTrain && lead && lane == 0) {
-    for (int i = 0; i < 4; ++i)
-      if (cnt[i]) atomicAdd(p.a.tr.stats + i, (unsigned long long)cnt[i]);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<COLS>(tmem);
-  }
-}
 
 bool tc_supported(const nb_desc& d) {
   if (d.precision != NB_BF16) return false;
@@ -522,65 +12,36 @@ bool tc_supported(const nb_desc& d) {
 }
 
 // NB_TRACE builds: device buffer set by nb_debug_set_trace (tools/trace_fwd.py).
-static unsigned long long* g_trace_buffer = nullptr;
+unsigned long long* g_trace_buffer = nullptr;
+static bool g_no_fold = false;
 #ifdef NB_TRACE
 extern "C" void nb_debug_set_trace(void* dev_buf) { g_trace_buffer = (unsigned long long*)dev_buf; }
 #endif
 
-template <int W, int LC, int H0C, int H1C, int MODE>
-static cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
-  constexpr int NSLOT = TcPlan<W>::NSLOT, WPS = TcPlan<W>::WPS;
-  TcParams p;
-  p.a = a;
-  p.packed = m->packed;
-  p.pl = m->pl;
-  p.d0 = m->d0;
-  p.L = m->d.hidden_layers;
-  p.nh = m->d.n_heads;
-  p.ha0 = m->d.head_after[0];
-  p.ha1 = m->d.head_after[1];
-  p.num_tiles = (a.n + kTile - 1) / kTile;
-  p.trace = g_trace_buffer;
-  if (p.num_tiles == 0) return cudaSuccess;
-  // weights | barriers + tmem slot | head-partial exchange | counters | staging;
-  // requesting >= 116 KB also forces one CTA per SM (TMEM is allocated whole)
-  size_t smem = ((m->pl.bytes + 15) & ~15u) + 8 * (2 + 2 * NSLOT) + 16 +
-                sizeof(float) * NSLOT * 2 * 4 * 32 * 3 + 4 * NSLOT * WPS * 12 + 8 * 2 * NSLOT +
-                sizeof(float) * NSLOT * 2 * kTile * 8 + NSLOT * 2 * kTile;
-  smem = std::max<size_t>(smem, 116 * 1024);
-  auto kern = k_fwd_tc<W, LC, H0C, H1C, MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
-  kern<<<grid, NSLOT * WPS * 32, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <int W, int LC, int H0C, int H1C>
-static cudaError_t launch_tc_modes(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
-  if (mode == kForward) return launch_tc_wm<W, LC, H0C, H1C, kForward>(m, a, st);
-  if (mode == kCalibrate) return launch_tc_wm<W, LC, H0C, H1C, kCalibrate>(m, a, st);
-  if (mode == kTrain) return launch_tc_wm<W, LC, H0C, H1C, kTrain>(m, a, st);
-  return launch_tc_wm<W, LC, H0C, H1C, kScore>(m, a, st);
-}
-
-// Specialised (fully unrolled) kernels for the BASELINE.json architectures;
-// every other architecture runs the generic instantiation (LC = 0).
+// Specialised (fully unrolled, compile-time d0) kernels for the BASELINE.json
+// architectures; every other architecture runs the generic instantiation
+// (LC = 0, run-time d0, L and heads).  Both fold the biases into the MMAs
+// whenever layer 1's K = 16 operand has room for them (2 d0 + 3 <= 16).
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
   const nb_desc& d = m->d;
   const int h0 = d.n_heads > 0 ? d.head_after[0] : 0, h1 = d.n_heads > 1 ? d.head_after[1] : 0;
-  if (d.width == 64 && d.hidden_layers == 4 && d.n_heads == 0)
-    return launch_tc_modes<64, 4, 0, 0>(m, mode, a, st);
-  if (d.width == 128 && d.hidden_layers == 4 && d.n_heads == 0)
-    return launch_tc_modes<128, 4, 0, 0>(m, mode, a, st);
-  if (d.width == 128 && d.hidden_layers == 6 && h0 == 2 && h1 == 4)
-    return launch_tc_modes<128, 6, 2, 4>(m, mode, a, st);
+  const bool bf = m->pl.bias_l0 != 0;
+  if (bf && d.width == 64 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 3)
+    return launch_tc_w64l4_d3(m, mode, a, st, !g_no_fold);
+  if (bf && d.width == 128 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 6)
+    return launch_tc_w128l4_d6(m, mode, a, st, !g_no_fold);
+  if (bf && d.width == 128 && d.hidden_layers == 6 && h0 == 2 && h1 == 4 && m->d0 == 4)
+    return launch_tc_w128l6h24_d4(m, mode, a, st, !g_no_fold);
+  const bool fold = bf && !g_no_fold;
   switch (d.width) {
-    case 32: return launch_tc_modes<32, 0, 0, 0>(m, mode, a, st);
-    case 64: return launch_tc_modes<64, 0, 0, 0>(m, mode, a, st);
-    case 128: return launch_tc_modes<128, 0, 0, 0>(m, mode, a, st);
+    case 32: return launch_tc_gen32(m, mode, a, st, fold);
+    case 64: return launch_tc_gen64(m, mode, a, st, fold);
+    case 128: return launch_tc_gen128(m, mode, a, st, fold);
   }
   return cudaErrorInvalidValue;
 }
+
+// Measurement switch (tools/quickbench.py NB_NO_FOLD=1): epilogue-bias kernels.
+extern "C" void nb_debug_set_no_fold(int v) { g_no_fold = v != 0; }
 
 }  // namespace nb

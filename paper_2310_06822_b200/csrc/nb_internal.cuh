@@ -32,6 +32,14 @@ struct PackLayout {
   uint32_t off_bout;           // fp32 (padded to 16 B)
   uint32_t off_u[2];           // fp32 [W] per head
   uint32_t off_c;              // fp32 [2] head biases (padded)
+  uint32_t core_bytes;         // the image up to here (what the training kernels copy)
+  // Bias-as-MMA blocks (pairs == 1 only, DESIGN.md §6 "bias folding"): layer
+  // l >= 1 has an [W][16] K-major B image whose k = 0, 1, 2 columns hold the
+  // exact bf16 split hi + mid + lo of b_l (a ones block in TMEM is its A);
+  // layer 0's image holds the same split in columns 2 d0 .. 2 d0 + 2 when
+  // bias_l0 != 0 (the in-kernel encoder puts ones there).
+  uint32_t off_bb[kMaxLayers];
+  uint32_t bias_l0;
   uint32_t bytes;              // one image, multiple of 16
   uint32_t pairs;              // 1, or 2 for CTA-pair widths (2 images, each with W/2 rows)
 };

@@ -70,6 +70,16 @@ struct PackArgs {
   int W, L, d0, nh;
 };
 
+// Piece j of the exact three-way bf16 split b = hi + mid + lo (each piece is
+// exactly representable in bf16; their fp32 sum is b for normal-range b).
+__device__ __forceinline__ float bias_piece(float b, int j) {
+  const float hi = __bfloat162float(__float2bfloat16_rn(b));
+  const float r = b - hi;
+  const float mid = __bfloat162float(__float2bfloat16_rn(r));
+  const float lo = __bfloat162float(__float2bfloat16_rn(r - mid));
+  return j == 0 ? hi : (j == 1 ? mid : lo);
+}
+
 __global__ void k_pack_bf16(PackArgs a) {
   const int W = a.W;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -84,6 +94,8 @@ __global__ void k_pack_bf16(PackArgs a) {
       if (l == 0) {
         int src = k < a.d0 ? k : (k < 2 * a.d0 ? k - a.d0 : -1);
         v = src >= 0 ? a.theta[a.po.W[0] + (int64_t)n * a.d0 + src] : 0.f;
+        const int j = k - 2 * a.d0;  // bias split columns (the encoder's ones)
+        if (a.pl.bias_l0 && j >= 0 && j < 3) v = bias_piece(a.theta[a.po.b[0] + n], j);
       } else {
         v = a.theta[a.po.W[l] + (int64_t)n * W + k];
       }
@@ -92,6 +104,17 @@ __global__ void k_pack_bf16(PackArgs a) {
           (__nv_bfloat16*)(a.out + (size_t)img_i * a.pl.bytes + a.pl.off_w[l]);
       int64_t off = (int64_t)(nl / 8) * (K / 8) * 64 + (k / 8) * 64 + (nl % 8) * 8 + (k % 8);
       img[off] = __float2bfloat16_rn(v);
+    }
+  }
+  // bias-as-MMA blocks of layers l >= 1: [W][16] K-major, k = 0..2 = split of b_l
+  for (int l = 1; l < a.L; ++l) {
+    if (!a.pl.off_bb[l]) continue;
+    __nv_bfloat16* img = (__nv_bfloat16*)(a.out + a.pl.off_bb[l]);
+    for (int64_t e = tid; e < (int64_t)W * kEncK; e += stride) {
+      const int n = (int)(e / kEncK), k = (int)(e % kEncK);
+      const float v = k < 3 ? bias_piece(a.theta[a.po.b[l] + n], k) : 0.f;
+      img[(int64_t)(n / 8) * (kEncK / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 + (k % 8)] =
+          __float2bfloat16_rn(v);
     }
   }
   float* bias = (float*)(a.out + a.pl.off_bias);

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   static_assert(NSLOT * (W + W / 2) <= 512, "TMEM plan");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
+  const uint32_t bar_off = (p.pl.core_bytes + 15u) & ~15u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);  // [0] weights, [1+s] acc_full
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -58,9 +58,9 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
       mbar_init(smem_u32(bars), 1);
       for (int s = 0; s < NSLOT; ++s) mbar_init(smem_u32(bars + 1 + s), 1);
       fence_barrier_init();
-      mbar_arrive_expect_tx(smem_u32(bars), p.pl.bytes);
-      for (uint32_t off = 0; off < p.pl.bytes; off += 32768u)
-        bulk_g2s(sbase + off, p.packed + off, min(32768u, p.pl.bytes - off), smem_u32(bars));
+      mbar_arrive_expect_tx(smem_u32(bars), p.pl.core_bytes);
+      for (uint32_t off = 0; off < p.pl.core_bytes; off += 32768u)
+        bulk_g2s(sbase + off, p.packed + off, min(32768u, p.pl.core_bytes - off), smem_u32(bars));
     }
     __syncwarp();
     tmem_alloc<COLS>(smem_u32(tmem_slot));
@@ -379,7 +379,7 @@ size_t train_tc_scratch_bytes(const nb_model* m, int64_t n) {
 
 template <int W>
 static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) {
-  size_t smem = ((m->pl.bytes + 15) & ~15u) + 64;
+  size_t smem = ((m->pl.core_bytes + 15) & ~15u) + 64;
   smem = std::max<size_t>(smem, 116 * 1024);
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -355,3 +355,26 @@ def test_full_size_sampled_parity(name):
     assert np.abs(sigmoid(zs) - sigmoid(zr)).max() <= 2e-2
     ze = oracle.forward(a, th.double().numpy(), qs, oracle.BF16_EMU)
     assert (np.abs(zs - ze) < BAND).mean() > 0.99
+
+
+@pytest.mark.gpu
+def test_score_async_matches_score():
+    """nb_score_async (pinned host and device destinations) gives nb_score's counts."""
+    import torch
+
+    cfg = nbgen.CONFIGS["c2"]
+    n = 128 * 300 + 5
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n, device="cuda:0")
+    g = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, 0)
+    y = g.label(cfg.kind, q)
+    m = nb.Model(nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), "bf16"), 0)
+    m.set_params(nbgen.init_params(cfg) * 2.5)
+    m.calibrate(q, y)
+    ref = m.score(q, y)
+    h = torch.zeros(9, dtype=torch.int64).pin_memory()
+    d = torch.zeros(9, dtype=torch.int64, device="cuda:0")
+    m.score_async(q, y, h)
+    m.score_async(q, y, d)
+    torch.cuda.synchronize()
+    assert m.counts_dict(h) == ref and m.counts_dict(d) == ref
+    assert ref["fn"] == 0

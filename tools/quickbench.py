@@ -9,6 +9,8 @@ import torch
 import nbgen
 import paper_2310_06822_b200 as nb
 
+if os.environ.get("NB_NO_FOLD"):
+    nb.lib().nb_debug_set_no_fold(1)
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 logn = int(sys.argv[2]) if len(sys.argv) > 2 else 22
 cfg = nbgen.CONFIGS[name]
