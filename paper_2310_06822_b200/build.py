@@ -45,8 +45,8 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, extra: list[str]) -> tuple[str, str]:
-    obj = os.path.join(OBJ, src + ".o")
+def _compile(src: str, extra: list[str], objdir: str = OBJ) -> tuple[str, str]:
+    obj = os.path.join(objdir, src + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + \
         [os.path.join(INCLUDE, "nb.h"), __file__]
     if not _stale(obj, deps):
@@ -61,26 +61,39 @@ def _compile(src: str, extra: list[str]) -> tuple[str, str]:
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), name: str = "",
+          only: tuple = ()) -> str:
+    """Build libnb.so; `defines` (e.g. ("NB_W64_NSLOT=5",)) + `name` build a
+    measurement variant libnb_<name>.so from its own object directory; with
+    `only`, just those sources get the defines (the rest link the main objects)."""
+    objdir = os.path.join(OBJ, name) if name else OBJ
+    lib = os.path.join(HERE, f"libnb_{name}.so") if name else LIB
+    os.makedirs(objdir, exist_ok=True)
     if force:
-        for f in os.listdir(OBJ):
-            os.remove(os.path.join(OBJ, f))
+        for f in os.listdir(objdir):
+            if os.path.isfile(os.path.join(objdir, f)):
+                os.remove(os.path.join(objdir, f))
+    dflags = [f"-D{d}" for d in defines]
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        futs = {s: ex.submit(_compile, s, e) for s, e in SOURCES.items()}
+        futs = {s: ex.submit(_compile, s, e + (dflags if not only or s in only else []),
+                             objdir if not only or s in only else OBJ)
+                for s, e in SOURCES.items()}
         objs = []
         for s, f in futs.items():
             obj, log = f.result()
             objs.append(obj)
             if verbose and log:
                 print(f"[{s}]\n{log}")
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    nm = next((a[7:] for a in sys.argv[1:] if a.startswith("--name=")), "")
+    on = tuple(x for a in sys.argv[1:] if a.startswith("--only=") for x in a[7:].split(","))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, name=nm, only=on))

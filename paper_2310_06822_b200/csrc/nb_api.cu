@@ -254,7 +254,9 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->grad, sizeof(float) * m->P);
   A((void**)&m->packed, (size_t)m->pl.bytes * m->pl.pairs);
   A((void**)&m->d_tau, sizeof(float) * 4);
-  A((void**)&m->d_counts, sizeof(unsigned long long) * 16);
+  // [0, 9) kernel counters (kept zero between launches by the finalising CTA),
+  // [16, 25) finalised totals, [32, 41) a block that stays zero
+  A((void**)&m->d_counts, sizeof(unsigned long long) * 48);
   A((void**)&m->d_keys, sizeof(unsigned int) * 4);
   A((void**)&m->d_flags, sizeof(unsigned int) * 4);
   A((void**)&m->d_loss, sizeof(double) * 2);
@@ -428,6 +430,9 @@ static FwdArgs base_args(const nb_model* m, const float* q, const uint8_t* y, in
   a.n = n;
   for (int k = 0; k < 3; ++k) a.tau[k] = m->tau[k];
   a.counts = m->d_counts;
+  a.fin_out = m->d_counts + 16;  // finalised totals (score mode)
+  a.ticket = m->d_flags + 2;     // last-CTA ticket, zero between launches
+  a.fin_add = 0;
   a.keys = m->d_keys;
   a.flags = m->d_flags;
   return a;
@@ -490,15 +495,29 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
   if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
-  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
+  unsigned long long* fin = m->d_counts + 16;
   if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
-  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
+  else NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
+  if (m->comm && comm_allreduce_u64_sum(m, fin, kNumCounters, s)) return NB_E_NCCL;
   unsigned long long* hc = m->h_pinned;
-  NB_CUDA(cudaMemcpyAsync(hc, m->d_counts, sizeof(unsigned long long) * kNumCounters,
+  NB_CUDA(cudaMemcpyAsync(hc, fin, sizeof(unsigned long long) * kNumCounters,
                           cudaMemcpyDeviceToHost, s));
   NB_CUDA(cudaStreamSynchronize(s));
   counts_out(hc, out);
   return take_flags(m, s, NB_OK);
+}
+
+// Device-visible address of `out` (device memory, or pinned host memory mapped
+// into the device's address space); NULL if the device cannot write it.
+static void* device_view(void* out) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, out) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return out;
+  if (at.type == cudaMemoryTypeHost) return at.devicePointer;
+  return nullptr;
 }
 
 nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, int64_t n,
@@ -507,12 +526,23 @@ nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, i
   nb_model* m = const_cast<nb_model*>(m_);
   if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
   DeviceGuard g(m->device);
+  void* dout = device_view(out);
+  if (!dout) return set_error("nb_score_async: out must be device or pinned host memory"), NB_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
-  if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
-  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
   // the device counter order is the nb_counts field order (tp fp fn tn exit[4] nonfinite)
-  NB_CUDA(cudaMemcpyAsync(out, m->d_counts, sizeof(nb_counts), cudaMemcpyDefault, s));
+  if (n == 0) {
+    NB_CUDA(cudaMemcpyAsync(out, m->d_counts + 32, sizeof(nb_counts), cudaMemcpyDefault, s));
+    return NB_OK;
+  }
+  FwdArgs a = base_args(m, q, y, n);
+  if (!m->comm) {  // one launch: the last CTA writes the totals straight into `out`
+    a.fin_out = (unsigned long long*)dout;
+    NB_CUDA(launch_forward_any(m, kScore, a, s));
+    return NB_OK;
+  }
+  NB_CUDA(launch_forward_any(m, kScore, a, s));
+  if (comm_allreduce_u64_sum(m, a.fin_out, kNumCounters, s)) return NB_E_NCCL;
+  NB_CUDA(cudaMemcpyAsync(out, a.fin_out, sizeof(nb_counts), cudaMemcpyDefault, s));
   return NB_OK;
 }
 
@@ -534,7 +564,8 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
     }
     m->stage_rows = chunk;
   }
-  NB_CUDA(cudaMemsetAsync(m->d_counts, 0, sizeof(unsigned long long) * kNumCounters, s));
+  unsigned long long* fin = m->d_counts + 16;
+  NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
   // the copy stream may only start once the counters are reset / prior work done
   NB_CUDA(cudaEventRecord(m->ev_done[0], s));
   NB_CUDA(cudaEventRecord(m->ev_done[1], s));
@@ -548,12 +579,14 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
     NB_CUDA(cudaMemcpyAsync(m->stage_y[b], yh + r0, rows, cudaMemcpyHostToDevice, m->copy_stream));
     NB_CUDA(cudaEventRecord(m->ev_copy[b], m->copy_stream));
     NB_CUDA(cudaStreamWaitEvent(s, m->ev_copy[b], 0));
-    NB_CUDA(launch_forward_any(m, kScore, base_args(m, m->stage_q[b], m->stage_y[b], rows), s));
+    FwdArgs a = base_args(m, m->stage_q[b], m->stage_y[b], rows);
+    a.fin_add = 1;  // every chunk's last CTA adds its totals into fin
+    NB_CUDA(launch_forward_any(m, kScore, a, s));
     NB_CUDA(cudaEventRecord(m->ev_done[b], s));
   }
-  if (m->comm && comm_allreduce_u64_sum(m, m->d_counts, kNumCounters, s)) return NB_E_NCCL;
+  if (m->comm && comm_allreduce_u64_sum(m, fin, kNumCounters, s)) return NB_E_NCCL;
   unsigned long long* hc = m->h_pinned;
-  NB_CUDA(cudaMemcpyAsync(hc, m->d_counts, sizeof(unsigned long long) * kNumCounters,
+  NB_CUDA(cudaMemcpyAsync(hc, fin, sizeof(unsigned long long) * kNumCounters,
                           cudaMemcpyDeviceToHost, s));
   NB_CUDA(cudaStreamSynchronize(s));
   counts_out(hc, out);

@@ -80,6 +80,27 @@ __device__ __forceinline__ void flush_warp(WarpAcc& acc, int nh, unsigned long l
 #pragma unroll
     for (int i = 0; i < kNumCounters; ++i)
       if (acc.c[i]) atomicAdd(counts + i, (unsigned long long)acc.c[i]);
+    __threadfence();
+  }
+}
+
+// Last-CTA finalisation of the fused score counters (row a5).  Called by one
+// thread per CTA after a __syncthreads that follows all of the CTA's counter
+// atomics (each flushing lane fenced them).  The CTA drawing the last ticket
+// moves the totals to a.fin_out and re-arms counters and ticket for the next
+// launch (stream order makes that safe).
+__device__ __forceinline__ void finalize_counts(const FwdArgs& a) {
+  __threadfence();
+  const unsigned int t = atomicAdd(a.ticket, 1u);
+  if (t == gridDim.x * gridDim.y * gridDim.z - 1) {
+    __threadfence();
+    for (int i = 0; i < kNumCounters; ++i) {
+      const unsigned long long v = atomicExch(a.counts + i, 0ull);
+      if (a.fin_add) atomicAdd(a.fin_out + i, v);
+      else a.fin_out[i] = v;
+    }
+    __threadfence();  // (host-mapped fin_out is visible at kernel completion)
+    atomicExch(a.ticket, 0u);
   }
 }
 
@@ -138,6 +159,22 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
           "r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
+}
+
+// Shared-memory flag / counter operations with acquire-release semantics at
+// CTA scope (the chunk hand-off of the fused forward kernel).
+__device__ __forceinline__ uint32_t atom_add_acqrel_smem(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t ld_acquire_smem(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_smem(uint32_t addr, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 // One lane of the (converged) warp returns true (elect.sync).

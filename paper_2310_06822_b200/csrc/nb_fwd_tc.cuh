@@ -174,15 +174,20 @@ __device__ __forceinline__ void flush_smem(uint32_t* cnt, uint32_t (&key)[3], in
     if (nh == 0) cnt[6] = cnt[2] + cnt[3];           // final-negative
     for (int i = 0; i < kNumCounters; ++i)
       if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
+    __threadfence();
   }
 }
 
+#ifndef NB_W64_NSLOT  // measurement variants: build.py -DNB_W64_NSLOT=4 -DNB_W64_WPS=8
+#define NB_W64_NSLOT 5
+#define NB_W64_WPS 4
+#endif
 template <int W>
 struct TcPlan;
 template <>
 struct TcPlan<32> { static constexpr int NSLOT = 4, WPS = 4, COLS = 256; };
 template <>
-struct TcPlan<64> { static constexpr int NSLOT = 5, WPS = 4, COLS = 512; };
+struct TcPlan<64> { static constexpr int NSLOT = NB_W64_NSLOT, WPS = NB_W64_WPS, COLS = 512; };
 template <>
 struct TcPlan<128> { static constexpr int NSLOT = 2, WPS = 8, COLS = 512; };
 
@@ -234,6 +239,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   uint64_t* sbars = reinterpret_cast<uint64_t*>(ctr + NEPI * 12);            // [NSLOT][2]
   float* qst = reinterpret_cast<float*>(sbars + 2 * NSLOT);                  // [NSLOT][2][128*8]
   uint8_t* yst = reinterpret_cast<uint8_t*>(qst + NSLOT * 2 * kTile * 8);   // [NSLOT][2][128]
+  // UMMA B descriptors of every layer's weight image ([0, 8)) and bias block
+  // ([8, 16)), computed once so the issuing lane only loads them
+  uint64_t* dtab = reinterpret_cast<uint64_t*>(yst + NSLOT * 2 * kTile);
   auto stage_bar = [&](int s, int b) { return smem_u32(sbars + 2 * s + b); };
   auto q_stage = [&](int s, int b) { return qst + (size_t)(2 * s + b) * kTile * 8; };
   auto y_stage = [&](int s, int b) { return yst + (size_t)(2 * s + b) * kTile; };
@@ -266,6 +274,11 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     tmem_alloc<COLS>(smem_u32(tmem_slot));
   }
   for (int i = threadIdx.x; i < NEPI * 12; i += blockDim.x) ctr[i] = 0u;
+  if (threadIdx.x < kMaxLayers) {
+    const int l = threadIdx.x;
+    dtab[l] = make_sdesc(sbase + p.pl.off_w[l], 128u, (l == 0 ? kEncK / 8u : W / 8u) * 128u);
+    dtab[kMaxLayers + l] = make_sdesc(sbase + p.pl.off_bb[l], 128u, (kEncK / 8u) * 128u);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -305,7 +318,10 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   uint32_t ph = 0;
   const int nl = 1 + NH;
   const uint32_t slot_bar = 1u + (uint32_t)s;              // all WPS warps of the slot
-  const uint32_t half_bar = 8u + (uint32_t)(s * 4 + qw);   // the 2 warps of a row quarter
+  // the 2 warps of a row quarter combine their column halves; with too many
+  // slots for private named barriers the whole slot meets instead
+  constexpr bool kPairBars = 8 + NSLOT * 4 <= 16;
+  const uint32_t half_bar = kPairBars ? 8u + (uint32_t)(s * 4 + qw) : slot_bar;
   const int d0 = D0C ? D0C : p.d0;
   const uint32_t idesc = make_idesc_bf16(128, W);
 
@@ -321,12 +337,11 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         const uint32_t d = tmem + acc_col(s);
         const uint32_t a = tmem + a_col(s);
         if (l == 0) {
-          mma_ts(d, a, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u), idesc, 0u);
+          mma_ts(d, a, dtab[0], idesc, 0u);
         } else {
           if (BF)  // bias first: D = ones * [hi mid lo]^T, then D += A W^T
-            mma_ts(d, tmem + kOnesCol, make_sdesc(sbase + p.pl.off_bb[l], 128u, (kEncK / 8u) * 128u),
-                   idesc, 0u);
-          const uint64_t bdesc = make_sdesc(sbase + p.pl.off_w[l], 128u, (W / 8u) * 128u);
+            mma_ts(d, tmem + kOnesCol, dtab[kMaxLayers + l], idesc, 0u);
+          const uint64_t bdesc = dtab[l];
 #pragma unroll
           for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
             mma_ts(d, a + kk * 8u, bdesc + (uint64_t)(kk * 16u), idesc, (BF || kk > 0u) ? 1u : 0u);
@@ -460,18 +475,18 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
           const int o = 32 * c;
-          if (l == h0) {
+          // head vectors: 16-B aligned (pack layout, col0 % 32 == 0) -> LDS.128
+          auto dot = [&](float& sa, float& sb, const float* w) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(e0a, e0b, t[i], t[i + 1], u0[o + i], u0[o + i + 1]);
-          }
-          if (l == h1) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(e1a, e1b, t[i], t[i + 1], u1[o + i], u1[o + i + 1]);
-          }
-          if (last) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) fma2(z0, z1, t[i], t[i + 1], wout[o + i], wout[o + i + 1]);
-          }
+            for (int i = 0; i < 32; i += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(w + o + i);
+              fma2(sa, sb, t[i], t[i + 1], w4.x, w4.y);
+              fma2(sa, sb, t[i + 2], t[i + 3], w4.z, w4.w);
+            }
+          };
+          if (l == h0) dot(e0a, e0b, u0);
+          if (l == h1) dot(e1a, e1b, u1);
+          if (last) dot(z0, z1, wout);
         }
       }
       if (!last) {
@@ -494,7 +509,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         xb[1] = e[0];
         xb[2] = e[1];
       }
-      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "n"(64) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "n"(kPairBars ? 64 : WPS * 32) : "memory");
       if (lead) {
         z += xb[0];
         e[0] += xb[1];
@@ -562,6 +577,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     tc_fence_after();
     tmem_dealloc<COLS>(tmem);
   }
+  if (MODE == kScore && warp == 1 && lane == 0 && p.a.ticket) finalize_counts(p.a);
 }
 
 // Trace buffer of NB_TRACE builds (defined in nb_fwd_tc.cu).
@@ -588,7 +604,7 @@ inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   p.pl.bytes = img;
   size_t smem = ((img + 15) & ~15u) + 8 * (2 + 2 * NSLOT) + 16 +
                 sizeof(float) * NSLOT * 2 * 4 * 32 * 3 + 4 * NSLOT * WPS * 12 + 8 * 2 * NSLOT +
-                sizeof(float) * NSLOT * 2 * kTile * 8 + NSLOT * 2 * kTile;
+                sizeof(float) * NSLOT * 2 * kTile * 8 + NSLOT * 2 * kTile + 16 * 8;
   smem = std::max<size_t>(smem, 116 * 1024);
   auto kern = k_fwd_tc<W, LC, H0C, H1C, MODE, D0C, BF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -126,6 +126,12 @@ struct FwdArgs {
   float* prob;
   float tau[3];
   unsigned long long* counts;
+  // a5 finalisation (kScore): when ticket != NULL the last CTA to finish moves
+  // the totals to fin_out (plain store, or atomicAdd when fin_add) and
+  // re-zeroes `counts` and the ticket, so a launch needs no memset or copy
+  unsigned long long* fin_out;
+  unsigned int* ticket;
+  int fin_add;
   unsigned int* keys;
   unsigned int* flags;
   TrainArgs tr;

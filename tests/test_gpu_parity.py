@@ -378,3 +378,14 @@ def test_score_async_matches_score():
     torch.cuda.synchronize()
     assert m.counts_dict(h) == ref and m.counts_dict(d) == ref
     assert ref["fn"] == 0
+    # repeated launches re-arm the in-kernel finalisation (counters start at 0)
+    for _ in range(3):
+        m.score_async(q, y, h)
+    torch.cuda.synchronize()
+    assert m.counts_dict(h) == ref and m.score(q, y) == ref
+    # n = 0 writes zeros; pageable host memory is rejected
+    m.score_async(q[:0], y[:0], h)
+    torch.cuda.synchronize()
+    assert all(v == 0 for v in h.tolist())
+    with pytest.raises(ValueError):
+        m.score_async(q, y, torch.zeros(9, dtype=torch.int64))

@@ -26,24 +26,32 @@ TRACE_LIB = os.path.join(ROOT, "paper_2310_06822_b200", "libnb_trace.so")
 
 
 def build_trace():
-    objs = []
+    import concurrent.futures as cf
+
     tdir = os.path.join(B.OBJ, "trace")
     os.makedirs(tdir, exist_ok=True)
-    for src, extra in B.SOURCES.items():
+
+    def one(item):
+        src, extra = item
         obj = os.path.join(tdir, src + ".o")
         lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
         cmd = [B.NVCC] + lang + B.ARCH + B.COMMON + extra + ["-DNB_TRACE", "-c",
                                                               os.path.join(B.CSRC, src), "-o", obj]
         subprocess.check_call(cmd, stderr=subprocess.DEVNULL)
-        objs.append(obj)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(B.SOURCES)) as ex:
+        objs = list(ex.map(one, B.SOURCES.items()))
     subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-o", TRACE_LIB] + objs + ["-ldl"])
 
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     logn = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    if not os.path.exists(TRACE_LIB):
+    if not os.path.exists(TRACE_LIB) or "--rebuild" in sys.argv:
         build_trace()
+        if "--build-only" in sys.argv:
+            return
     nb.LIB_PATH = TRACE_LIB
     L = nb.lib()
     L.nb_debug_set_trace.argtypes = [C.c_void_p]
@@ -64,6 +72,9 @@ def main():
     torch.cuda.synchronize()
     ev = [row for row in buf.view(-1, 2).cpu().tolist() if row[0] != 0]
     cnt = len(ev)
+    import json
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(ev, open(os.path.join(ROOT, "gpurun_out", f"trace_{name}_{logn}.json"), "w"))
     ev.sort()
     t0 = ev[0][0]
     # per (slot, layer-sequence) latencies
