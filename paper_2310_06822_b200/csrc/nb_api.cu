@@ -254,9 +254,9 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->grad, sizeof(float) * m->P);
   A((void**)&m->packed, (size_t)m->pl.bytes * m->pl.pairs);
   A((void**)&m->d_tau, sizeof(float) * 4);
-  // [0, 9) kernel counters (kept zero between launches by the finalising CTA),
-  // [16, 25) finalised totals, [32, 41) a block that stays zero
-  A((void**)&m->d_counts, sizeof(unsigned long long) * 48);
+  // kernel counters i * kCtrStride (kept zero between launches by the
+  // finalising CTA), finalised totals at kFinOff, a zero block at kZeroOff
+  A((void**)&m->d_counts, sizeof(unsigned long long) * 256);
   A((void**)&m->d_keys, sizeof(unsigned int) * 4);
   A((void**)&m->d_flags, sizeof(unsigned int) * 4);
   A((void**)&m->d_loss, sizeof(double) * 2);
@@ -430,7 +430,7 @@ static FwdArgs base_args(const nb_model* m, const float* q, const uint8_t* y, in
   a.n = n;
   for (int k = 0; k < 3; ++k) a.tau[k] = m->tau[k];
   a.counts = m->d_counts;
-  a.fin_out = m->d_counts + 16;  // finalised totals (score mode)
+  a.fin_out = m->d_counts + kFinOff;  // finalised totals (score mode)
   a.ticket = m->d_flags + 2;     // last-CTA ticket, zero between launches
   a.fin_add = 0;
   a.keys = m->d_keys;
@@ -495,7 +495,7 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
   if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned long long* fin = m->d_counts + 16;
+  unsigned long long* fin = m->d_counts + kFinOff;
   if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
   else NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
   if (m->comm && comm_allreduce_u64_sum(m, fin, kNumCounters, s)) return NB_E_NCCL;
@@ -531,7 +531,7 @@ nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, i
   cudaStream_t s = (cudaStream_t)stream;
   // the device counter order is the nb_counts field order (tp fp fn tn exit[4] nonfinite)
   if (n == 0) {
-    NB_CUDA(cudaMemcpyAsync(out, m->d_counts + 32, sizeof(nb_counts), cudaMemcpyDefault, s));
+    NB_CUDA(cudaMemcpyAsync(out, m->d_counts + kZeroOff, sizeof(nb_counts), cudaMemcpyDefault, s));
     return NB_OK;
   }
   FwdArgs a = base_args(m, q, y, n);
@@ -564,7 +564,7 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
     }
     m->stage_rows = chunk;
   }
-  unsigned long long* fin = m->d_counts + 16;
+  unsigned long long* fin = m->d_counts + kFinOff;
   NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
   // the copy stream may only start once the counters are reset / prior work done
   NB_CUDA(cudaEventRecord(m->ev_done[0], s));

@@ -79,28 +79,53 @@ __device__ __forceinline__ void flush_warp(WarpAcc& acc, int nh, unsigned long l
     if (nh == 0) acc.c[7] = acc.c[0] + acc.c[1], acc.c[6] = acc.c[2] + acc.c[3];
 #pragma unroll
     for (int i = 0; i < kNumCounters; ++i)
-      if (acc.c[i]) atomicAdd(counts + i, (unsigned long long)acc.c[i]);
-    __threadfence();
+      if (acc.c[i]) atomicAdd(counts + i * kCtrStride, (unsigned long long)acc.c[i]);
   }
 }
 
-// Last-CTA finalisation of the fused score counters (row a5).  Called by one
-// thread per CTA after a __syncthreads that follows all of the CTA's counter
-// atomics (each flushing lane fenced them).  The CTA drawing the last ticket
-// moves the totals to a.fin_out and re-arms counters and ticket for the next
-// launch (stream order makes that safe).
+// CTA-level count flush (score mode): one warp sums the per-warp shared-memory
+// counters ctr[w * 12 + i] of all nwarps warps and adds each total with ONE
+// atomic per CTA (exit bin 3 = tp + fp, and bin 2 = fn + tn without heads).
+__device__ __forceinline__ void flush_cta_counts(const uint32_t* ctr, int nwarps, int nh,
+                                                 unsigned long long* counts) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v = 0;
+  if (lane < kNumCounters)
+    for (int w = 0; w < nwarps; ++w) v += ctr[w * 12 + lane];
+  const uint32_t c0 = __shfl_sync(0xFFFFFFFFu, v, 0), c1 = __shfl_sync(0xFFFFFFFFu, v, 1);
+  const uint32_t c2 = __shfl_sync(0xFFFFFFFFu, v, 2), c3 = __shfl_sync(0xFFFFFFFFu, v, 3);
+  if (lane == 7) v = c0 + c1;
+  if (lane == 6 && nh == 0) v = c2 + c3;
+  if (lane < kNumCounters && v) atomicAdd(counts + lane * kCtrStride, (unsigned long long)v);
+}
+
+// Last-CTA finalisation of the fused score counters (row a5).  Called by all
+// 32 lanes of one warp per CTA after a __syncthreads that follows all of the
+// CTA's counter atomics.  Lane 0's fence is cumulative over the writes the
+// barrier made visible to it, so the ticket orders the whole CTA's counts.
+// The CTA drawing the last ticket moves the totals to a.fin_out (one lane per
+// counter) and re-arms counters and ticket for the next launch (stream order
+// makes that safe).
 __device__ __forceinline__ void finalize_counts(const FwdArgs& a) {
-  __threadfence();
-  const unsigned int t = atomicAdd(a.ticket, 1u);
+  const int lane = threadIdx.x & 31;
+  unsigned int t = 0;
+  if (lane == 0) {
+    __threadfence();
+    t = atomicAdd(a.ticket, 1u);
+  }
+  t = __shfl_sync(0xFFFFFFFFu, t, 0);
   if (t == gridDim.x * gridDim.y * gridDim.z - 1) {
     __threadfence();
-    for (int i = 0; i < kNumCounters; ++i) {
-      const unsigned long long v = atomicExch(a.counts + i, 0ull);
-      if (a.fin_add) atomicAdd(a.fin_out + i, v);
-      else a.fin_out[i] = v;
+    if (lane < kNumCounters) {
+      const unsigned long long v = atomicExch(a.counts + lane * kCtrStride, 0ull);
+      if (a.fin_add) atomicAdd(a.fin_out + lane, v);
+      else a.fin_out[lane] = v;
     }
-    __threadfence();  // (host-mapped fin_out is visible at kernel completion)
-    atomicExch(a.ticket, 0u);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();  // (host-mapped fin_out is visible at kernel completion)
+      atomicExch(a.ticket, 0u);
+    }
   }
 }
 

@@ -174,7 +174,6 @@ __device__ __forceinline__ void flush_smem(uint32_t* cnt, uint32_t (&key)[3], in
     if (nh == 0) cnt[6] = cnt[2] + cnt[3];           // final-negative
     for (int i = 0; i < kNumCounters; ++i)
       if (cnt[i]) atomicAdd(counts + i, (unsigned long long)cnt[i]);
-    __threadfence();
   }
 }
 
@@ -361,9 +360,14 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
     const uint32_t qb = (uint32_t)(kTile * d0 * 4);
     const uint32_t bar = stage_bar(s, b);
-    mbar_arrive_expect_tx(bar, qb + (MODE != kForward ? (uint32_t)kTile : 0u));
+#ifdef NB_EXP_NOY  // measurement variant: labels not loaded
+    constexpr bool kY = false;
+#else
+    constexpr bool kY = MODE != kForward;
+#endif
+    mbar_arrive_expect_tx(bar, qb + (kY ? (uint32_t)kTile : 0u));
     bulk_g2s(smem_u32(q_stage(s, b)), p.a.q + t * kTile * d0, qb, bar);
-    if (MODE != kForward) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
+    if (kY) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
   };
   uint32_t sph[2] = {0u, 0u};
   int ycur = 0;
@@ -378,7 +382,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         const float* qs = q_stage(s, b) + rit * d0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
+#ifndef NB_EXP_NOY
         ycur = MODE != kForward ? (int)y_stage(s, b)[rit] : 0;
+#endif
       } else {
         const int64_t r = t * kTile + rit;
         const bool v = r < n;
@@ -560,13 +566,14 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
         }
       } else {
+#ifndef NB_EXP_NOCLS  // measurement variant: no classification
         classify_row_smem<MODE, NHC>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+#endif
       }
     }
     tile = next;
   }
-  if ((MODE == kCalibrate || MODE == kScore) && lead)
-    flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
+  if (MODE == kCalibrate && lead) flush_smem<MODE>(cnt, key, NH, p.a.counts, p.a.keys);
   if (MODE == kTrain && lead && lane == 0) {
     for (int i = 0; i < 4; ++i)
       if (cnt[i]) atomicAdd(p.a.tr.stats + i, (unsigned long long)cnt[i]);
@@ -577,7 +584,10 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     tc_fence_after();
     tmem_dealloc<COLS>(tmem);
   }
-  if (MODE == kScore && warp == 1 && lane == 0 && p.a.ticket) finalize_counts(p.a);
+  if (MODE == kScore && warp == 1) flush_cta_counts(ctr, NEPI, NH, p.a.counts);
+#ifndef NB_EXP_NOFIN  // measurement variant: no count finalisation
+  if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a);
+#endif
 }
 
 // Trace buffer of NB_TRACE builds (defined in nb_fwd_tc.cu).

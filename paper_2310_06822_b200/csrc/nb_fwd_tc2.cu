@@ -399,11 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
         if (lane == 0 && mk != 0xFFFFFFFFu) atomicMin(p.a.keys + k, mk);
       }
     }
-    if (MODE == kScore && lane == 0) {
-      for (int i = 0; i < kNumCounters; ++i)
-        if (cnt[i]) atomicAdd(p.a.counts + i, (unsigned long long)cnt[i]);
-      __threadfence();
-    }
+
   }
   tc_fence_before();
   __syncthreads();
@@ -412,7 +408,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
-  if (MODE == kScore && warp == 1 && lane == 0 && p.a.ticket) finalize_counts(p.a);
+  if (MODE == kScore && warp == 1) flush_cta_counts(ctr, NWARP, NH, p.a.counts);
+  if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a);
 }
 
 bool tc2_supported(const nb_desc& d) {

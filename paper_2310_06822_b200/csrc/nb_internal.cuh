@@ -16,6 +16,9 @@ constexpr int kMaxLayers = 8;
 constexpr int kTile = 128;          // rows per MMA tile (M = 128)
 constexpr int kEncK = 16;           // layer-1 K after the bf16 (hi, lo) split
 constexpr int kNumCounters = 9;     // tp fp fn tn exit[4] nonfinite
+constexpr int kCtrStride = 16;      // device counters 128 B apart (one L2 line each)
+constexpr int kFinOff = kNumCounters * kCtrStride;  // nb_model::d_counts: finalised totals
+constexpr int kZeroOff = kFinOff + 16;              // ... and a block that stays zero
 constexpr uint32_t kFlagNonFinite = 1u, kFlagLabel = 2u;
 
 void set_error(const char* fmt, ...);
@@ -66,7 +69,7 @@ struct nb_model {
   uint8_t* packed = nullptr;  // bf16 packed image (pl.bytes)
   float tau[3] = {0, 0, 0};
   float* d_tau = nullptr;     // [3]
-  unsigned long long* d_counts = nullptr;  // [kNumCounters]
+  unsigned long long* d_counts = nullptr;  // counters (strided), totals, zeros: 256 words
   unsigned int* d_keys = nullptr;          // [3] order-preserving min keys
   unsigned int* d_flags = nullptr;         // sticky flags
   double* d_loss = nullptr;                // [1]

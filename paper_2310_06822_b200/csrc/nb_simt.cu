@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
   if (MODE != kForward) flush_warp<MODE>(acc, s.nh, a.counts, a.keys);
   if (MODE == kScore && a.ticket) {
     __syncthreads();
-    if (threadIdx.x == 0) finalize_counts(a);
+    if (threadIdx.x < 32) finalize_counts(a);
   }
 }
 

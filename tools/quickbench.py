@@ -17,7 +17,7 @@ import torch
 import nbgen
 import paper_2310_06822_b200 as nb
 
-if os.environ.get("NB_LIB"):  # measurement variant (build.py --name=...)
+if os.environ.get("NB_LIB", ""):  # measurement variant (build.py --name=...)
     nb.LIB_PATH = os.path.join(os.path.dirname(nb.LIB_PATH), f"libnb_{os.environ['NB_LIB']}.so")
 if os.environ.get("NB_NO_FOLD"):
     nb.lib().nb_debug_set_no_fold(1)
@@ -30,7 +30,7 @@ g = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, 0)
 y = g.label(cfg.kind, q)
 m = nb.Model(nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after), cfg.precision), 0)
 m.set_params(nbgen.init_params(cfg) * 2.5)
-m.calibrate(q, y)
+m.calibrate(q, y, allow_no_positives=bool(os.environ.get('NB_LIB', '')))
 flop = 2 * (cfg.record_floats * cfg.width + (cfg.hidden_layers - 1) * cfg.width ** 2 + cfg.width * (1 + cfg.n_heads))
 logits = torch.empty(n, 1 + cfg.n_heads, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
