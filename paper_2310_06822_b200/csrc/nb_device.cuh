@@ -86,6 +86,7 @@ __device__ __forceinline__ void flush_warp(WarpAcc& acc, int nh, unsigned long l
 // CTA-level count flush (score mode): one warp sums the per-warp shared-memory
 // counters ctr[w * 12 + i] of all nwarps warps and adds each total with ONE
 // atomic per CTA (exit bin 3 = tp + fp, and bin 2 = fn + tn without heads).
+// nh < 0: the counters are raw (tp, pred, pos, ..., nonfinite); passed as is.
 __device__ __forceinline__ void flush_cta_counts(const uint32_t* ctr, int nwarps, int nh,
                                                  unsigned long long* counts) {
   const int lane = threadIdx.x & 31;
@@ -94,7 +95,7 @@ __device__ __forceinline__ void flush_cta_counts(const uint32_t* ctr, int nwarps
     for (int w = 0; w < nwarps; ++w) v += ctr[w * 12 + lane];
   const uint32_t c0 = __shfl_sync(0xFFFFFFFFu, v, 0), c1 = __shfl_sync(0xFFFFFFFFu, v, 1);
   const uint32_t c2 = __shfl_sync(0xFFFFFFFFu, v, 2), c3 = __shfl_sync(0xFFFFFFFFu, v, 3);
-  if (lane == 7) v = c0 + c1;
+  if (lane == 7 && nh >= 0) v = c0 + c1;
   if (lane == 6 && nh == 0) v = c2 + c3;
   if (lane < kNumCounters && v) atomicAdd(counts + lane * kCtrStride, (unsigned long long)v);
 }
@@ -106,7 +107,9 @@ __device__ __forceinline__ void flush_cta_counts(const uint32_t* ctr, int nwarps
 // The CTA drawing the last ticket moves the totals to a.fin_out (one lane per
 // counter) and re-arms counters and ticket for the next launch (stream order
 // makes that safe).
-__device__ __forceinline__ void finalize_counts(const FwdArgs& a) {
+// raw: the counters hold (tp, pred, pos, -, -, -, -, -, nonfinite) of a model
+// without exit heads; the totals are derived here with n = a.n valid rows.
+__device__ __forceinline__ void finalize_counts(const FwdArgs& a, bool raw = false) {
   const int lane = threadIdx.x & 31;
   unsigned int t = 0;
   if (lane == 0) {
@@ -116,8 +119,18 @@ __device__ __forceinline__ void finalize_counts(const FwdArgs& a) {
   t = __shfl_sync(0xFFFFFFFFu, t, 0);
   if (t == gridDim.x * gridDim.y * gridDim.z - 1) {
     __threadfence();
+    unsigned long long v = 0;
+    if (lane < kNumCounters) v = atomicExch(a.counts + lane * kCtrStride, 0ull);
+    if (raw) {
+      const unsigned long long tp = __shfl_sync(0xFFFFFFFFu, v, 0), pred = __shfl_sync(0xFFFFFFFFu, v, 1);
+      const unsigned long long pos = __shfl_sync(0xFFFFFFFFu, v, 2), n = (unsigned long long)a.n;
+      const unsigned long long t[kNumCounters] = {tp, pred - tp, pos - tp, n - pred - pos + tp,
+                                                  0ull, 0ull, n - pred, pred, 0ull};
+#pragma unroll
+      for (int i = 0; i < kNumCounters - 1; ++i)
+        if (lane == i) v = t[i];
+    }
     if (lane < kNumCounters) {
-      const unsigned long long v = atomicExch(a.counts + lane * kCtrStride, 0ull);
       if (a.fin_add) atomicAdd(a.fin_out + lane, v);
       else a.fin_out[lane] = v;
     }

@@ -127,7 +127,20 @@ __device__ __forceinline__ void classify_row_smem(uint32_t* cnt, uint32_t (&key)
       if (nh > 1) key[2] = min(key[2], dkey(e[1]));
     }
   }
-  if (MODE == kScore) {
+  if (MODE == kScore && NHC == 0) {
+    // no exit heads: count the raw masks tp = pred & y, pred, pos = y (and
+    // non-finite); finalize_counts derives fp, fn, tn and the bins from them
+    const unsigned full = 0xFFFFFFFFu;
+    const uint32_t bp = __ballot_sync(full, valid && z >= tau[0]);
+    const uint32_t by = __ballot_sync(full, valid && y != 0);
+    const uint32_t bn = __ballot_sync(full, valid && !isfinite(z));
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(cnt + 0, (uint32_t)__popc(bp & by));
+      atomicAdd(cnt + 1, (uint32_t)__popc(bp));
+      atomicAdd(cnt + 2, (uint32_t)__popc(by));
+      if (bn) atomicAdd(cnt + 8, (uint32_t)__popc(bn));
+    }
+  } else if (MODE == kScore) {
     const unsigned full = 0xFFFFFFFFu;
     bool pass0 = true, pass1 = true;
     if (nh > 0) pass0 = e[0] >= tau[1];
@@ -584,9 +597,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     tc_fence_after();
     tmem_dealloc<COLS>(tmem);
   }
-  if (MODE == kScore && warp == 1) flush_cta_counts(ctr, NEPI, NH, p.a.counts);
+  if (MODE == kScore && warp == 1) flush_cta_counts(ctr, NEPI, NHC == 0 ? -1 : NH, p.a.counts);
 #ifndef NB_EXP_NOFIN  // measurement variant: no count finalisation
-  if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a);
+  if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a, NHC == 0);
 #endif
 }
 
