@@ -10,10 +10,11 @@
 //     same shared-memory weight image the forward uses; writes delta images.
 //  3. k_dw_tc: dW_l = delta_l^T [h_{l-1} | 1] summed over row tiles with
 //     tcgen05.mma (A, B both MN-major from row-tile images; the constant "ones"
-//     block gives db_l = sum delta_l), per-CTA partials in fp32.
+//     block gives db_l = sum delta_l), per-CTA partials in fp32.  ONE launch
+//     covers every layer's job (blockIdx.y = job, blockIdx.x = CTA of the job).
 //  4. k_dw_reduce: fixed-order sum of the CTA partials into the canonical
-//     gradient blob (deterministic); then NCCL allreduce, Adam, bf16 re-pack
-//     (nb_api.cu).
+//     gradient blob (deterministic, all jobs, coalesced); then NCCL allreduce,
+//     Adam, bf16 re-pack (nb_api.cu).
 #include <cuda_bf16.h>
 
 #include "nb_device.cuh"
@@ -179,10 +180,25 @@ struct DwJob {
   int m_off;     // first A feature of this job (M half for w = 256)
   const uint8_t* b_img;
   int fb;        // features of the B image (<= 256)
-  float* partial;  // [gridDim.x][128][fb + 16]
+  // reduction of this job's partials into the gradient blob (k_dw_reduce)
+  int kind;      // 0: W[m][k] <- D[m][k], b[m] <- D[m][fb]
+                 // 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
+                 // 2: head row `row`: v[j] <- D[row][j], c <- D[row][fb]
+  int rows, row, d0, in;
+  float* w_out;
+  float* b_out;
+};
+constexpr int kMaxDwJobs = kMaxLayers + 3;
+constexpr int kDwCols = kDwMaxN + 16;  // partial columns per CTA (features + ones block)
+// partial of CTA c of job j, column col, D row m: [(j * cpj + c) * kDwCols + col] * 128 + m
+struct DwJobs {
+  DwJob job[kMaxDwJobs];
+  int njobs, cpj;
+  float* partial;
 };
 
-__global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
+__global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs js, int64_t num_tiles) {
+  const DwJob& j = js.job[blockIdx.y];
   extern __shared__ __align__(1024) uint8_t smem[];
   // A tile: 128 features (16 groups) x 128 rows = 32 KB; B tile + ones: (fb + 16) x 256 B
   const uint32_t a_bytes = 128u * 256u;
@@ -218,7 +234,7 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t per = (num_tiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = blockIdx.x * per, t1 = min(num_tiles, t0 + per);
+  const int64_t t0 = min(num_tiles, blockIdx.x * per), t1 = min(num_tiles, t0 + per);
   const int fa_job = min(128, j.fa - j.m_off);
   const uint32_t a_copy = (uint32_t)fa_job * 256u;  // bytes of this job's A features per tile
   const uint32_t idesc = make_idesc_bf16(128, j.fb, 1, 1);
@@ -272,16 +288,17 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
     mbar_wait(smem_u32(bars + 2), (uint32_t)((ntl - 1) & 1));
   }
   tc_fence_after();
-  // epilogue: thread = row m of D (lane quarter = warp), N fp32 columns
+  // epilogue: thread = row m of D (lane quarter = warp), N fp32 columns; the
+  // partial is column-major ([col][128 rows]) so a warp's stores are coalesced
   const int m = warp * 32 + lane;
-  float* out = j.partial + ((int64_t)blockIdx.x * 128 + m) * N;
+  float* out = js.partial + ((int64_t)(blockIdx.y * js.cpj + blockIdx.x) * kDwCols) * 128 + m;
   for (int c = 0; c < N; c += 16) {
     uint32_t v[32];
     if (c + 32 <= N) {
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) out[c + i] = t1 > t0 ? __uint_as_float(v[i]) : 0.f;
+      for (int i = 0; i < 32; ++i) out[(int64_t)(c + i) * 128] = t1 > t0 ? __uint_as_float(v[i]) : 0.f;
       c += 16;
     } else {
       uint32_t w[16];
@@ -294,7 +311,7 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
           : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) out[c + i] = t1 > t0 ? __uint_as_float(w[i]) : 0.f;
+      for (int i = 0; i < 16; ++i) out[(int64_t)(c + i) * 128] = t1 > t0 ? __uint_as_float(w[i]) : 0.f;
     }
   }
   tc_fence_before();
@@ -305,38 +322,44 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(DwJob j, int64_t num_tiles) {
   }
 }
 
-// Fixed-order reduction of the CTA partials into the gradient blob.
+// Fixed-order reduction of the CTA partials into the gradient blob, every job
+// at once (deterministic: CTA order 0..cpj-1).  One thread per output element,
+// D row m fastest, so a warp's partial loads are coalesced.
 //   kind 0: hidden layer l >= 2: W[m][k] <- D[m][k], b[m] <- D[m][fb]
 //   kind 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
 //   kind 2: head row `row` of the head-gradient image: v[j] <- D[row][j], c <- D[row][fb]
-struct DwReduce {
-  const float* partial;
-  int ncta, N, fb, kind, rows, m_off, row, d0, in;
-  float* w_out;  // weights (row-major [rows][in]) or head vector
-  float* b_out;
-};
-
-__global__ void k_dw_reduce(DwReduce r) {
-  const int per_row = r.in + 1;
-  const int total = r.kind == 2 ? per_row : r.rows * per_row;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int m = r.kind == 2 ? r.row : i / per_row;  // row of D
-    const int k = i % per_row;
-    float acc = 0.f;
-    for (int c = 0; c < r.ncta; ++c) {
-      const float* P = r.partial + ((int64_t)c * 128 + m) * r.N;
-      if (k == r.in) acc += P[r.fb];
-      else if (r.kind == 1) acc += P[k] + P[r.d0 + k];
-      else acc += P[k];
+__global__ void k_dw_reduce(const __grid_constant__ DwJobs js) {
+  int64_t base = 0;
+  for (int jj = 0; jj < js.njobs; ++jj) {
+    const DwJob& r = js.job[jj];
+    const int per_row = r.in + 1;
+    const int rows = r.kind == 2 ? 1 : r.rows;
+    const int64_t total = (int64_t)rows * per_row;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - base; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      if (i < 0) continue;
+      const int k = (int)(i / rows);            // output column (k == in: bias)
+      const int mi = (int)(i % rows);
+      const int m = r.kind == 2 ? r.row : mi;   // row of D
+      const int c0 = k == r.in ? r.fb : k;
+      const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : -1;
+      const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
+      float acc = 0.f;
+      for (int c = 0; c < js.cpj; ++c) {
+        const float* Pc = P + (int64_t)c * kDwCols * 128;
+        acc += Pc[(int64_t)c0 * 128];
+        if (c1 >= 0) acc += Pc[(int64_t)c1 * 128];
+      }
+      if (r.kind == 2) {
+        if (k == r.in) *r.b_out = acc;
+        else r.w_out[k] = acc;
+      } else {
+        const int mo = m + r.m_off;
+        if (k == r.in) r.b_out[mo] = acc;
+        else r.w_out[(int64_t)mo * r.in + k] = acc;
+      }
     }
-    if (r.kind == 2) {
-      if (k == r.in) *r.b_out = acc;
-      else r.w_out[k] = acc;
-    } else {
-      const int mo = m + r.m_off;
-      if (k == r.in) r.b_out[mo] = acc;
-      else r.w_out[(int64_t)mo * r.in + k] = acc;
-    }
+    base += total;
   }
 }
 
@@ -368,7 +391,7 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
   take(img_tile_bytes(128));
   t.hd_img = take(T * img_tile_bytes(8) + img_tile_bytes(128));
   t.g32 = take((size_t)T * kTile * 3 * sizeof(float));
-  t.partial = take((size_t)grid * 128 * (kDwMaxN + 16) * sizeof(float));
+  t.partial = take((size_t)grid * 128 * kDwCols * sizeof(float));  // njobs * cpj <= grid
   t.total = off;
   return t;
 }
@@ -388,12 +411,17 @@ static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-static cudaError_t run_dw(nb_model* m, const DwJob& j, int64_t T, int grid, cudaStream_t st) {
-  const size_t stage = 128 * 256 + (size_t)(j.fb + 16) * 256;
+static cudaError_t run_dw(const DwJobs& js, int64_t T, cudaStream_t st) {
+  int fbmax = 0;
+  for (int i = 0; i < js.njobs; ++i) fbmax = std::max(fbmax, js.job[i].fb);
+  const size_t stage = 128 * 256 + (size_t)(fbmax + 16) * 256;
   const size_t smem = 2 * stage + 64;
   cudaError_t e = cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_dw_tc<<<grid, 128, smem, st>>>(j, T);
+  k_dw_tc<<<dim3(js.cpj, js.njobs), 128, smem, st>>>(js, T);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_dw_reduce<<<64, 256, 0, st>>>(js);
   return cudaGetLastError();
 }
 
@@ -444,56 +472,37 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   bp.g32 = (float*)(base + tl.g32);
   if (n > 0) e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
   if (e != cudaSuccess) return e;
-  // 3 + 4. dW GEMM jobs and their deterministic reductions
-  float* partial = (float*)(base + tl.partial);
-  auto job = [&](const uint8_t* a_img, int fa, const uint8_t* b_img, int fb, DwReduce r) {
-    DwJob j{a_img, fa, 0, b_img, fb, partial};
-    cudaError_t e2 = cudaSuccess;
-    if (n > 0) e2 = run_dw(m, j, T, grid, st);
-    else e2 = cudaMemsetAsync(partial, 0, sizeof(float) * 128 * (fb + 16) * grid, st);
-    if (e2 != cudaSuccess) return e2;
-    r.partial = partial;
-    r.ncta = grid;
-    r.N = fb + 16;
-    r.fb = fb;
-    k_dw_reduce<<<64, 256, 0, st>>>(r);
-    return cudaGetLastError();
-  };
+  // 3 + 4. dW GEMM jobs (one launch) and their deterministic reduction (one launch)
+  DwJobs js{};
+  js.partial = (float*)(base + tl.partial);
   float* g = m->grad;
-  for (int l = 0; l < L && e == cudaSuccess; ++l) {
-    DwReduce r{};
-    r.rows = W;
-    r.w_out = g + m->po.W[l];
-    r.b_out = g + m->po.b[l];
-    if (l == 0) {
-      r.kind = 1;
-      r.d0 = d0;
-      r.in = d0;
-      e = job(base + tl.d_img[0], W, base + tl.x_img, 16, r);
-    } else {
-      r.kind = 0;
-      r.in = W;
-      e = job(base + tl.d_img[l], W, base + tl.h_img[l - 1], W, r);
-    }
+  auto add = [&](const uint8_t* a_img, int fa, const uint8_t* b_img, int fb, int kind, int rows,
+                 int row, int in, float* w_out, float* b_out) {
+    DwJob& j = js.job[js.njobs++];
+    j = DwJob{a_img, fa, 0, b_img, fb, kind, rows, row, d0, in, w_out, b_out};
+  };
+  for (int l = 0; l < L; ++l) {
+    if (l == 0)
+      add(base + tl.d_img[0], W, base + tl.x_img, 16, 1, W, 0, d0, g + m->po.W[0], g + m->po.b[0]);
+    else
+      add(base + tl.d_img[l], W, base + tl.h_img[l - 1], W, 0, W, 0, W, g + m->po.W[l], g + m->po.b[l]);
   }
-  // output head: row 0 of the head-gradient image against h_L
+  // output head: row 0 of the head-gradient image against h_L; exit heads: rows 1, 2
+  add(base + tl.hd_img, 8, base + tl.h_img[L - 1], W, 2, 1, 0, W, g + m->po.wout, g + m->po.bout);
+  for (int k = 0; k < m->d.n_heads; ++k)
+    add(base + tl.hd_img, 8, base + tl.h_img[m->d.head_after[k] - 1], W, 2, 1, 1 + k, W,
+        g + m->po.u[k], g + m->po.c[k]);
+  js.cpj = (int)std::max<int64_t>(1, std::min<int64_t>(T, m->num_sms / js.njobs));
   if (e == cudaSuccess) {
-    DwReduce r{};
-    r.kind = 2;
-    r.row = 0;
-    r.in = W;
-    r.w_out = g + m->po.wout;
-    r.b_out = g + m->po.bout;
-    e = job(base + tl.hd_img, 8, base + tl.h_img[L - 1], W, r);
-  }
-  for (int k = 0; k < m->d.n_heads && e == cudaSuccess; ++k) {
-    DwReduce r{};
-    r.kind = 2;
-    r.row = 1 + k;
-    r.in = W;
-    r.w_out = g + m->po.u[k];
-    r.b_out = g + m->po.c[k];
-    e = job(base + tl.hd_img, 8, base + tl.h_img[m->d.head_after[k] - 1], W, r);
+    if (n > 0) {
+      e = run_dw(js, T, st);
+    } else {  // empty batch: zero gradient
+      e = cudaMemsetAsync(js.partial, 0, sizeof(float) * 128 * kDwCols * js.cpj * js.njobs, st);
+      if (e == cudaSuccess) {
+        k_dw_reduce<<<64, 256, 0, st>>>(js);
+        e = cudaGetLastError();
+      }
+    }
   }
   return e;
 }

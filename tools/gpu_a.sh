@@ -1,3 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-for i in 1 2; do timeout 300 python tools/quickbench.py c2 22; done > gpurun_out/quick.log 2>&1
-cat gpurun_out/pytest_gpu.log gpurun_out/quick.log
+timeout 600 python bench.py --steps 20 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+cat gpurun_out/pytest_gpu.log; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'], d['train'])"
