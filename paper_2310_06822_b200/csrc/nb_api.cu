@@ -259,8 +259,8 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->d_counts, sizeof(unsigned long long) * 256);
   A((void**)&m->d_keys, sizeof(unsigned int) * 4);
   A((void**)&m->d_flags, sizeof(unsigned int) * 4);
-  A((void**)&m->d_loss, sizeof(double) * 2);
-  A((void**)&m->d_stats, sizeof(unsigned long long) * 8);
+  A((void**)&m->d_loss, 64);  // [0, 16): loss (double), [16, 48): batch stats (4 x u64)
+  if (e == cudaSuccess) m->d_stats = reinterpret_cast<unsigned long long*>(m->d_loss + 2);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&m->h_pinned, 256);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -298,7 +298,6 @@ void nb_model_destroy(nb_model* m) {
   cudaFree(m->d_keys);
   cudaFree(m->d_flags);
   cudaFree(m->d_loss);
-  cudaFree(m->d_stats);
   cudaFree(m->train_scratch);
   for (int i = 0; i < 2; ++i) {
     cudaFree(m->stage_q[i]);
@@ -621,8 +620,7 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
     if (e != cudaSuccess) return set_error("train scratch: %s", cudaGetErrorString(e)), NB_E_OOM;
     m->train_scratch_bytes = need;
   }
-  NB_CUDA(cudaMemsetAsync(m->d_loss, 0, sizeof(double), s));
-  NB_CUDA(cudaMemsetAsync(m->d_stats, 0, sizeof(unsigned long long) * 4, s));
+  NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
   if (tc)
     NB_CUDA(launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s));
   else
@@ -630,8 +628,8 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   if (m->comm) {
     if (comm_allreduce_f32_sum(m, m->grad, m->P, s)) return NB_E_NCCL;
   }
-  NB_CUDA(launch_adam(m, lr, s));
-  if (tc) NB_CUDA(launch_pack_bf16(m, s));
+  if (tc) NB_CUDA(launch_adam_pack(m, lr, s));
+  else NB_CUDA(launch_adam(m, lr, s));
   if (stats) {
     if (m->comm) {
       if (comm_allreduce_f64_sum(m, m->d_loss, 1, s)) return NB_E_NCCL;

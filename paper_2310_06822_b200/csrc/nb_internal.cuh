@@ -159,6 +159,7 @@ bool train_tc_supported(const nb_desc& d);
 size_t train_tc_scratch_bytes(const nb_model* m, int64_t n);
 size_t train_simt_scratch_bytes(const nb_model* m, int64_t n);
 cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s);
+cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s);  // Adam + bf16 re-pack
 cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, uint8_t* y,
                          cudaStream_t s);
 cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);

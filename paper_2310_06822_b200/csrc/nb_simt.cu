@@ -572,6 +572,86 @@ __global__ void k_adam(float* __restrict__ th, float* __restrict__ m, float* __r
   }
 }
 
+// Adam fused with the bf16 re-pack: the thread that updates parameter i also
+// writes every packed copy of it (weight image element(s), fp32 tail entries,
+// bias split pieces) — the same values k_pack_bf16 would write; padding
+// positions of the image never change after the first full pack.
+__device__ __forceinline__ void store_bf16(uint8_t* img, int K, int n, int k, float v) {
+  reinterpret_cast<__nv_bfloat16*>(img)[(int64_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 +
+                                        (k % 8)] = __float2bfloat16_rn(v);
+}
+
+__global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
+                            const float* __restrict__ g, int64_t P, float lr_over_bc1,
+                            float inv_sqrt_bc2, float b1, float b2, float eps, PackArgs a) {
+  const int W = a.W, rows = W / (int)a.pl.pairs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float t = th[i] - lr_over_bc1 * mi / (sqrtf(vi) * inv_sqrt_bc2 + eps);
+    th[i] = t;
+    // ---- re-pack parameter i
+    auto fp32_tail = [&](uint32_t off_bytes) {  // replicated in every pair image
+      for (uint32_t im = 0; im < a.pl.pairs; ++im)
+        *reinterpret_cast<float*>(a.out + (size_t)im * a.pl.bytes + off_bytes) = t;
+    };
+    bool done = false;
+    for (int l = 0; l < a.L && !done; ++l) {
+      const int in = l == 0 ? a.d0 : W;
+      const int64_t ow = a.po.W[l], ob = a.po.b[l];
+      if (i >= ow && i < ow + (int64_t)W * in) {
+        const int n = (int)((i - ow) / in), k = (int)((i - ow) % in);
+        uint8_t* img = a.out + (size_t)(n / rows) * a.pl.bytes + a.pl.off_w[l];
+        store_bf16(img, (int)a.pl.k_of[l], n % rows, k, t);
+        if (l == 0) store_bf16(img, (int)a.pl.k_of[0], n % rows, a.d0 + k, t);  // lo copy
+        done = true;
+      } else if (i >= ob && i < ob + W) {
+        const int n = (int)(i - ob);
+        fp32_tail(a.pl.off_bias + 4u * (uint32_t)(l * W + n));
+        if (l == 0 && a.pl.bias_l0) {
+          uint8_t* img = a.out + a.pl.off_w[0];
+          for (int j = 0; j < 3; ++j) store_bf16(img, kEncK, n, 2 * a.d0 + j, bias_piece(t, j));
+        } else if (l > 0 && a.pl.off_bb[l]) {
+          uint8_t* img = a.out + a.pl.off_bb[l];
+          for (int j = 0; j < 3; ++j) store_bf16(img, kEncK, n, j, bias_piece(t, j));
+        }
+        done = true;
+      }
+    }
+    if (done) continue;
+    if (i >= a.po.wout && i < a.po.wout + W) fp32_tail(a.pl.off_wout + 4u * (uint32_t)(i - a.po.wout));
+    else if (i == a.po.bout) fp32_tail(a.pl.off_bout);
+    for (int k = 0; k < a.nh; ++k) {
+      if (i >= a.po.u[k] && i < a.po.u[k] + W) fp32_tail(a.pl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
+      else if (i == a.po.c[k]) fp32_tail(a.pl.off_c + 4u * (uint32_t)k);
+    }
+  }
+}
+
+cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
+  m->step += 1;
+  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  const double bc1 = 1.0 - pow(b1, (double)m->step), bc2 = 1.0 - pow(b2, (double)m->step);
+  PackArgs a;
+  a.theta = m->theta;
+  a.out = m->packed;
+  a.pl = m->pl;
+  a.po = m->po;
+  a.W = m->d.width;
+  a.L = m->d.hidden_layers;
+  a.d0 = m->d0;
+  a.nh = m->d.n_heads;
+  int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
+  k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P,
+                                     (float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1,
+                                     (float)b2, (float)eps, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s) {
   m->step += 1;
   const double b1 = 0.9, b2 = 0.999, eps = 1e-8;

@@ -389,3 +389,23 @@ def test_score_async_matches_score():
     assert all(v == 0 for v in h.tolist())
     with pytest.raises(ValueError):
         m.score_async(q, y, torch.zeros(9, dtype=torch.int64))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_fused_adam_repack_matches_full_pack(name):
+    """The training step's fused Adam + bf16 re-pack leaves exactly the image a
+    full pack of the updated fp32 master builds: logits after 3 steps equal the
+    logits of a fresh model given the same parameters (bit for bit)."""
+    cfg = nbgen.CONFIGS[name]
+    B = 1 << 12
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 9))
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), cfg.space_dim, DEV)
+    for t in range(3):
+        qt = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, t * B, B, device=f"cuda:{DEV}")
+        m.train_step(qt, g.label(cfg.kind, qt), alpha=10.0 * (t + 1))
+    th = m.get_params()
+    m2 = nb.Model(desc_of(cfg), DEV)
+    m2.set_params(th)
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 128 * 40 + 3, device=f"cuda:{DEV}")
+    assert torch.equal(m.forward(q), m2.forward(q))
