@@ -17,6 +17,8 @@
 //     Adam, bf16 re-pack (nb_api.cu).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "nb_device.cuh"
 #include "nb_internal.cuh"
 
@@ -87,22 +89,44 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   uint32_t ph = 0;
   const int64_t G = gridDim.x;
 
-  for (int64_t tile = blockIdx.x + (int64_t)s * G; tile < p.num_tiles; tile += NSLOT * G) {
-    const int64_t r = tile * kTile + rit;
-    const bool valid = r < p.n;
-    const float gz = valid ? p.g32[r * 3] : 0.f;
-    const float ge0 = valid ? p.g32[r * 3 + 1] : 0.f, ge1 = valid ? p.g32[r * 3 + 2] : 0.f;
+  // Global-memory latency is kept off the per-layer chain: each thread's h row
+  // of the next layer (ReLU masks) and the next tile's dL/dz are loaded one
+  // step ahead into registers.
+  constexpr int HW = W / 8;  // uint4 per h row
+  auto load_h = [&](uint4 (&h)[HW], int l1, int64_t t) {  // h_{l1} row of tile t (l1 1-based)
+    const uint8_t* hrow = p.h_img[l1 - 1] + t * img_tile_bytes(W);
+#pragma unroll
+    for (int q = 0; q < HW; ++q) h[q] = *reinterpret_cast<const uint4*>(hrow + img_off(rit, q));
+  };
+  auto load_g = [&](float (&gg)[3], int64_t t) {
+    const int64_t r = t * kTile + rit;
+    const bool valid = t < p.num_tiles && r < p.n;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gg[k] = valid ? p.g32[r * 3 + k] : 0.f;
+  };
+  uint4 hcur[HW], hnext[HW];
+  float gcur[3], gnext[3];
+  int64_t tile = blockIdx.x + (int64_t)s * G;
+  if (tile < p.num_tiles) {
+    load_h(hcur, p.L, tile);
+    load_g(gcur, tile);
+  }
+  for (; tile < p.num_tiles; tile += NSLOT * G) {
+    const int64_t next = tile + NSLOT * G;
+    load_g(gnext, next);
+    const float gz = gcur[0], ge0 = gcur[1], ge1 = gcur[2];
     // l (1-based) runs L .. 1; the value in flight is dL/dh_l
     for (int l = p.L; l >= 1; --l) {
       uint32_t v[32];
-      const uint8_t* hrow = p.h_img[l - 1] + tile * img_tile_bytes(W);
       uint8_t* drow = p.d_img[l - 1] + tile * img_tile_bytes(W);
+      if (l > 1) load_h(hnext, l - 1, tile);
+      else if (next < p.num_tiles) load_h(hnext, p.L, next);
       if (l < p.L) {
         mbar_wait(acc_full, ph);
         ph ^= 1u;
         tc_fence_after();
       }
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < W / 32; ++c) {
         if (l < p.L) {
           tmem_ld32(trow + acc + 32u * c, v);
@@ -120,7 +144,7 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
         uint32_t pk[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint4 hv = *reinterpret_cast<const uint4*>(hrow + img_off(rit, 4 * c + q));
+          const uint4 hv = hcur[4 * c + q];
           const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -136,6 +160,8 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         if (l >= 2) tmem_st16(trow + acol + 16u * c, pk);
       }
+#pragma unroll
+      for (int q = 0; q < HW; ++q) hcur[q] = hnext[q];
       if (l >= 2) {
         // delta_l is in TMEM: MMA dL/dh_{l-1} = delta_l W_l (K = out of layer l)
         tmem_wait_st();
@@ -157,6 +183,8 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
         }
       }
     }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gcur[k] = gnext[k];
   }
   tc_fence_before();
   __syncthreads();
@@ -194,36 +222,40 @@ constexpr int kDwCols = kDwMaxN + 16;  // partial columns per CTA (features + on
 struct DwJobs {
   DwJob job[kMaxDwJobs];
   int njobs, cpj;
+  int nst;        // TMA pipeline stages (<= kDwMaxStages)
+  uint32_t stage; // bytes per stage (A 32 KB + B of the widest job + ones block)
   float* partial;
 };
+constexpr int kDwMaxStages = 6;
 
 __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs js, int64_t num_tiles) {
   const DwJob& j = js.job[blockIdx.y];
   extern __shared__ __align__(1024) uint8_t smem[];
-  // A tile: 128 features (16 groups) x 128 rows = 32 KB; B tile + ones: (fb + 16) x 256 B
+  // stage: A tile 128 features (16 groups) x 128 rows = 32 KB, then B + ones: (fb + 16) x 256 B
   const uint32_t a_bytes = 128u * 256u;
-  const uint32_t b_bytes = (uint32_t)(j.fb + 16) * 256u;
-  const uint32_t stage = a_bytes + b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * stage);  // [0,1] full, [2] mma done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const uint32_t stage = js.stage;
+  const int NST = js.nst;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * stage);  // [st] full, [NST + st] empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kDwMaxStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = smem_u32(smem);
   const int N = j.fb + 16;
-  // ones block after each stage's B image: feature fb = 1.0 for every row
-  for (int st = 0; st < 2; ++st) {
+  for (int st = 0; st < NST; ++st) {
+    // ones block after each stage's B image: feature fb = 1.0 for every row
     uint8_t* ones = smem + st * stage + a_bytes + j.fb * 256;
     for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) {
       const int r = i / 16, f = i % 16;
       *reinterpret_cast<uint16_t*>(ones + img_off(r, f / 8) + (f % 8) * 2) = f == 0 ? 0x3F80 : 0;
     }
     // rows of A beyond fa are read but never used: keep them finite
-    for (int i = threadIdx.x * 4; i < (int)a_bytes; i += blockDim.x * 4)
-      if (i >= j.fa * 256 || j.m_off > 0) *reinterpret_cast<uint32_t*>(smem + st * stage + i) = 0u;
+    const int z0 = (j.m_off > 0 ? 0 : j.fa * 256) / 16;
+    for (int i = z0 + threadIdx.x; i < (int)a_bytes / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem + st * stage)[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < 3; ++i) mbar_init(smem_u32(bars + i), 1);
+      for (int i = 0; i < 2 * NST; ++i) mbar_init(smem_u32(bars + i), 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -239,29 +271,43 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
   const uint32_t a_copy = (uint32_t)fa_job * 256u;  // bytes of this job's A features per tile
   const uint32_t idesc = make_idesc_bf16(128, j.fb, 1, 1);
   const uint32_t idesc1 = make_idesc_bf16(128, 16, 1, 1);
+  const int64_t ntl = t1 - t0;
   if (warp == 0) {
-    auto issue_copy = [&](int64_t t, int st) {
+    // producer (lane 0) runs up to NST tiles ahead of the MMAs; a stage is
+    // refilled once the commit of the tile that last used it has arrived
+    auto issue_copy = [&](int i, int st, uint32_t eph) {
+      if (i >= NST) mbar_wait(smem_u32(bars + NST + st), eph);
       const uint32_t bar = smem_u32(bars + st);
+      const int64_t t = t0 + i;
       mbar_arrive_expect_tx(bar, a_copy + (uint32_t)j.fb * 256u);
       bulk_g2s(sbase + st * stage, j.a_img + t * img_tile_bytes(j.fa) + (int64_t)j.m_off * 256,
                a_copy, bar);
       bulk_g2s(sbase + st * stage + a_bytes, j.b_img + t * img_tile_bytes(j.fb),
                (uint32_t)j.fb * 256u, bar);
     };
-    uint32_t ph[2] = {0u, 0u}, done_ph = 0;
-    if (lane == 0 && t0 < t1) issue_copy(t0, 0);
-    for (int64_t t = t0; t < t1; ++t) {
-      const int st = (int)((t - t0) & 1);
-      if (lane == 0 && t + 1 < t1) {
-        // the other stage is free once the previous tile's MMAs completed
-        if (t > t0) {
-          mbar_wait(smem_u32(bars + 2), done_ph);
-          done_ph ^= 1u;
+    // producer state (lane 0): next tile to copy, its stage and that stage's
+    // empty-barrier parity; consumer state: stage and full-barrier parity
+    int issued = 0, ist = 0, cst = 0;
+    uint32_t pround = 0, fph = 0;  // tile k = pround * NST + ist waits for commit (pround - 1)
+    for (int i = 0; i < (int)ntl; ++i) {
+      // NST - 1 tiles in flight: refilling the stage of tile i - 1 (whose MMAs
+      // may still run) is left to the next iteration
+      if (lane == 0) {
+        for (; issued < (int)ntl && issued < i + NST - 1; ++issued) {
+          issue_copy(issued, ist, (pround & 1u) ^ 1u);
+          if (++ist == NST) {
+            ist = 0;
+            ++pround;
+          }
         }
-        issue_copy(t + 1, st ^ 1);
       }
-      mbar_wait(smem_u32(bars + st), ph[st]);
-      ph[st] ^= 1u;
+      __syncwarp();
+      const int st = cst;
+      mbar_wait(smem_u32(bars + st), fph);
+      if (++cst == NST) {
+        cst = 0;
+        fph ^= 1u;
+      }
       tc_fence_after();
       if (elect_one()) {
         const uint32_t as = sbase + st * stage, bs = as + a_bytes;
@@ -271,21 +317,20 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
         const uint64_t od = make_sdesc(bs + (uint32_t)j.fb * 256u, 128u, 2048u);
 #pragma unroll
         for (uint32_t kk = 0; kk < 8; ++kk) {
-          const uint32_t acc = (t > t0 || kk > 0) ? 1u : 0u;
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
           mma_ss(tmem, ad + kk * 16u, bd + kk * 16u, idesc, acc);
           mma_ss(tmem + (uint32_t)j.fb, ad + kk * 16u, od + kk * 16u, idesc1, acc);
         }
-        mma_commit(smem_u32(bars + 2));
+        mma_commit(smem_u32(bars + NST + st));
       }
       __syncwarp();
     }
   }
   __syncthreads();
-  // wait for all MMAs: the final commit's phase
-  if (t1 > t0) {
-    const int64_t ntl = t1 - t0;
-    // warp 0 consumed (ntl - 1) completions; the last one has parity (ntl - 1) & 1
-    mbar_wait(smem_u32(bars + 2), (uint32_t)((ntl - 1) & 1));
+  // wait for all MMAs: the last tile's commit
+  if (ntl > 0) {
+    const int i = (int)ntl - 1;
+    mbar_wait(smem_u32(bars + NST + i % NST), (uint32_t)((i / NST) & 1));
   }
   tc_fence_after();
   // epilogue: thread = row m of D (lane quarter = warp), N fp32 columns; the
@@ -411,11 +456,15 @@ static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-static cudaError_t run_dw(const DwJobs& js, int64_t T, cudaStream_t st) {
+static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
   int fbmax = 0;
   for (int i = 0; i < js.njobs; ++i) fbmax = std::max(fbmax, js.job[i].fb);
-  const size_t stage = 128 * 256 + (size_t)(fbmax + 16) * 256;
-  const size_t smem = 2 * stage + 64;
+  js.stage = (uint32_t)(128 * 256 + (fbmax + 16) * 256);
+  const size_t fixed = 8 * 2 * kDwMaxStages + 16;
+  js.nst = (int)std::min<size_t>(kDwMaxStages, (227 * 1024 - fixed) / js.stage);  // >= 3
+  if (const char* ev = getenv("NB_DW_STAGES"))  // measurement override
+    js.nst = std::max(2, std::min(js.nst, atoi(ev)));
+  const size_t smem = (size_t)js.nst * js.stage + fixed;
   cudaError_t e = cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_dw_tc<<<dim3(js.cpj, js.njobs), 128, smem, st>>>(js, T);
