@@ -7,7 +7,7 @@
  *
  * Every function follows PAPER.md (arXiv 2310.06822) step by step, in fp64
  * unless stated; citations are PAPER.md line numbers (P:n) with the section.
- * Readings of silent/ambiguous points are DESIGN.md §2 (R1..R31).
+ * Readings of silent/ambiguous points are DESIGN.md §2 (R1..R36).
  *
  * Parity status of each function is listed in DESIGN.md §5; the only
  * "parity unpinned" item is a whole multi-step training trajectory.
