@@ -97,12 +97,17 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   pl->off_c = off; off += 16u;
   off = align_up(off, 128u);
   pl->core_bytes = off;
-  const bool fold = pl->pairs == 1 && d.precision == NB_BF16;
   const int d0 = (int)nb_record_floats(d.kind, d.space_dim);
+  const bool shared = pl->pairs == 2 && d.precision == NB_BF16 && 3 * (d.hidden_layers - 1) <= kEncK;
+  const bool fold = (pl->pairs == 1 && d.precision == NB_BF16) || shared;
   pl->bias_l0 = (fold && 2 * d0 + 3 <= kEncK) ? 1u : 0u;
-  for (int l = 0; l < kMaxLayers; ++l) {
-    pl->off_bb[l] = 0;
-    if (fold && l >= 1 && l < d.hidden_layers) {
+  pl->bb_shared = shared ? 1u : 0u;
+  for (int l = 0; l < kMaxLayers; ++l) pl->off_bb[l] = 0;
+  if (shared) {
+    pl->off_bb[0] = off;
+    off = align_up(off + rows * (uint32_t)kEncK * 2u, 128u);
+  } else {
+    for (int l = 1; fold && l < d.hidden_layers; ++l) {
       pl->off_bb[l] = off;
       off = align_up(off + W * (uint32_t)kEncK * 2u, 128u);
     }

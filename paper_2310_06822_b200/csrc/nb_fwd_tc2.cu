@@ -72,6 +72,7 @@ __device__ __forceinline__ void mma_commit2(uint32_t bar) {
       : "memory");
 }
 
+template <bool ONES>
 __device__ __forceinline__ void encode_cols2(const float* x, int d0, uint32_t (&col)[8]) {
   uint32_t h[8], l[8];
 #pragma unroll
@@ -90,6 +91,7 @@ __device__ __forceinline__ void encode_cols2(const float* x, int d0, uint32_t (&
       v = (k == j && j < d0) ? h[j] : v;
       v = (k == d0 + j && j < d0) ? l[j] : v;
     }
+    if (ONES && k >= 2 * d0 && k < 2 * d0 + 3) v = 0x3F80u;  // layer 1's bias columns (R35)
     e[k] = v;
   }
 #pragma unroll
@@ -150,7 +152,10 @@ __device__ __forceinline__ void classify2(uint32_t* cnt, uint32_t (&key)[3], boo
   if (valid && y > 1) atomicOr(flags, kFlagLabel);
 }
 
-template <int LC, int MODE>
+// BF: bias folding (R35) — layer 1's bias through the encoder's ones columns,
+// layer l >= 1's through one K = 16 MMA of a per-layer ones block in TMEM
+// (columns ONES0 + 8 (l - 1)) against the pair image's shared bias block.
+template <int LC, int MODE, bool BF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(const TcParams2 p) {
   constexpr int W = 256, NWARP = 16, CPT = 64;
   const int L = LC ? LC : p.L;
@@ -196,6 +201,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
   cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (BF) {  // ones block of hidden layer l: bf16 1.0 at k = 3 (l - 1) .. 3 (l - 1) + 2
+    if (warp < 4) {
+      for (int l = 1; l < (LC ? LC : p.L); ++l) {
+        uint32_t ones[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int k0 = 2 * c, k1 = 2 * c + 1, lo = 3 * (l - 1), hi = lo + 3;
+          ones[c] = ((k0 >= lo && k0 < hi) ? 0x3F80u : 0u) | ((k1 >= lo && k1 < hi) ? 0x3F800000u : 0u);
+        }
+        tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + 384u + 8u * (uint32_t)(l - 1), ones);
+      }
+      tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   mbar_wait(w_bar, 0);
 
   const int64_t n = p.a.n;
@@ -208,6 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
   const int rit = qw * 32 + lane;                  // row within this CTA's half tile
   const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
   const uint32_t ACOL = 256;                       // bf16 A operand columns [256, 384)
+  const uint32_t ONES0 = 384;                      // BF: ones blocks [384, 384 + 8 (L - 1))
   const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
   const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
   const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
@@ -238,10 +261,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
             mma_ts2(tmem, tmem + ACOL, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u),
                     idesc, 0u);
           } else {
+            if (BF)  // bias first: D = ones_l * [splits]^T, then D += A W^T
+              mma_ts2(tmem, tmem + ONES0 + 8u * (uint32_t)(l - 1),
+                      make_sdesc(sbase + p.pl.off_bb[0], 128u, (kEncK / 8u) * 128u), idesc, 0u);
             const uint64_t bd = make_sdesc(sbase + p.pl.off_w[l], 128u, (W / 8u) * 128u);
 #pragma unroll
             for (uint32_t kk = 0; kk < (uint32_t)W / 16u; ++kk)
-              mma_ts2(tmem, tmem + ACOL + kk * 8u, bd + (uint64_t)(kk * 16u), idesc, kk > 0u);
+              mma_ts2(tmem, tmem + ACOL + kk * 8u, bd + (uint64_t)(kk * 16u), idesc,
+                      (BF || kk > 0u) ? 1u : 0u);
           }
           mma_commit2(acc_full);
         }
@@ -280,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
         ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
       }
       uint32_t c[8];
-      encode_cols2(x, d0, c);
+      encode_cols2<BF>(x, d0, c);
       tmem_st8(trow + ACOL, c);
       tmem_wait_st();
     }
@@ -321,11 +348,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         float* t = reinterpret_cast<float*>(v + 32 * c);
+        if (!BF) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
-          add2p(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
-          add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias + 32 * c + i);
+            add2p(t[i], t[i + 1], t[i], t[i + 1], b4.x, b4.y);
+            add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
+          }
         }
         if (!last) {
           uint32_t pk[16];
@@ -417,7 +446,7 @@ bool tc2_supported(const nb_desc& d) {
          d.hidden_layers <= kMaxLayers;
 }
 
-template <int LC, int MODE>
+template <int LC, int MODE, bool BF>
 static cudaError_t launch_tc2_m(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
   TcParams2 p;
   p.a = a;
@@ -432,25 +461,27 @@ static cudaError_t launch_tc2_m(const nb_model* m, const FwdArgs& a, cudaStream_
   if (p.num_pairs == 0) return cudaSuccess;
   const size_t smem = ((m->pl.bytes + 15) & ~15u) + 8 * 6 + 16 + sizeof(float) * 2 * 3 * 128 * 3 +
                       4 * 16 * 12 + sizeof(float) * 2 * kTile * 8 + 2 * kTile;
-  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc2<LC, MODE>,
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc2<LC, MODE, BF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int pairs = (int)std::min<int64_t>(p.num_pairs, m->num_sms / 2);
-  k_fwd_tc2<LC, MODE><<<2 * pairs, 512, smem, st>>>(p);
+  k_fwd_tc2<LC, MODE, BF><<<2 * pairs, 512, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-template <int LC>
+template <int LC, bool BF>
 static cudaError_t launch_tc2_l(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
-  if (mode == kForward) return launch_tc2_m<LC, kForward>(m, a, st);
-  if (mode == kCalibrate) return launch_tc2_m<LC, kCalibrate>(m, a, st);
-  return launch_tc2_m<LC, kScore>(m, a, st);
+  if (mode == kForward) return launch_tc2_m<LC, kForward, BF>(m, a, st);
+  if (mode == kCalibrate) return launch_tc2_m<LC, kCalibrate, BF>(m, a, st);
+  return launch_tc2_m<LC, kScore, BF>(m, a, st);
 }
 
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
   if (mode == kTrain) return cudaErrorNotSupported;
-  if (m->d.hidden_layers == 4) return launch_tc2_l<4>(m, mode, a, st);
-  return launch_tc2_l<0>(m, mode, a, st);
+  const bool bf = m->pl.bias_l0 && m->pl.bb_shared;
+  if (m->d.hidden_layers == 4)
+    return bf ? launch_tc2_l<4, true>(m, mode, a, st) : launch_tc2_l<4, false>(m, mode, a, st);
+  return bf ? launch_tc2_l<0, true>(m, mode, a, st) : launch_tc2_l<0, false>(m, mode, a, st);
 }
 
 }  // namespace nb

@@ -43,6 +43,10 @@ struct PackLayout {
   // bias_l0 != 0 (the in-kernel encoder puts ones there).
   uint32_t off_bb[kMaxLayers];
   uint32_t bias_l0;
+  // CTA-pair images (pairs == 2): ONE shared [rows][16] bias block at
+  // off_bb[0] holds the split of every hidden layer l >= 1 in columns
+  // 3 (l - 1) .. 3 (l - 1) + 2 (a per-layer ones block in TMEM selects them)
+  uint32_t bb_shared;
   uint32_t bytes;              // one image, multiple of 16
   uint32_t pairs;              // 1, or 2 for CTA-pair widths (2 images, each with W/2 rows)
 };

@@ -106,8 +106,18 @@ __global__ void k_pack_bf16(PackArgs a) {
       img[off] = __float2bfloat16_rn(v);
     }
   }
+  // CTA-pair images: one shared bias block per image, layer l >= 1 in columns 3 (l - 1) + j
+  if (a.pl.bb_shared) {
+    for (int64_t e = tid; e < (int64_t)(a.L - 1) * W * 3; e += stride) {
+      const int l = 1 + (int)(e / (W * 3)), n = (int)((e / 3) % W), jj = (int)(e % 3);
+      __nv_bfloat16* img = (__nv_bfloat16*)(a.out + (size_t)(n / rows) * a.pl.bytes + a.pl.off_bb[0]);
+      const int nl = n % rows, k = 3 * (l - 1) + jj;
+      img[(int64_t)(nl / 8) * (kEncK / 8) * 64 + (k / 8) * 64 + (nl % 8) * 8 + (k % 8)] =
+          __float2bfloat16_rn(bias_piece(a.theta[a.po.b[l] + n], jj));
+    }
+  }
   // bias-as-MMA blocks of layers l >= 1: [W][16] K-major, k = 0..2 = split of b_l
-  for (int l = 1; l < a.L; ++l) {
+  for (int l = 1; l < a.L && !a.pl.bb_shared; ++l) {
     if (!a.pl.off_bb[l]) continue;
     __nv_bfloat16* img = (__nv_bfloat16*)(a.out + a.pl.off_bb[l]);
     for (int64_t e = tid; e < (int64_t)W * kEncK; e += stride) {
@@ -152,8 +162,8 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s) {
   // CTA-pair images: replicate the fp32 tail (biases, output, heads) of image 0
   for (uint32_t i = 1; i < m->pl.pairs && e == cudaSuccess; ++i)
     e = cudaMemcpyAsync(m->packed + (size_t)i * m->pl.bytes + m->pl.off_bias,
-                        m->packed + m->pl.off_bias, m->pl.bytes - m->pl.off_bias,
-                        cudaMemcpyDeviceToDevice, s);
+                        m->packed + m->pl.off_bias, m->pl.core_bytes - m->pl.off_bias,
+                        cudaMemcpyDeviceToDevice, s);  // (bias blocks differ per image)
   return e;
 }
 
@@ -612,12 +622,15 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
       } else if (i >= ob && i < ob + W) {
         const int n = (int)(i - ob);
         fp32_tail(a.pl.off_bias + 4u * (uint32_t)(l * W + n));
+        uint8_t* imgb = a.out + (size_t)(n / rows) * a.pl.bytes;  // the image holding row n
         if (l == 0 && a.pl.bias_l0) {
-          uint8_t* img = a.out + a.pl.off_w[0];
-          for (int j = 0; j < 3; ++j) store_bf16(img, kEncK, n, 2 * a.d0 + j, bias_piece(t, j));
+          for (int j = 0; j < 3; ++j)
+            store_bf16(imgb + a.pl.off_w[0], kEncK, n % rows, 2 * a.d0 + j, bias_piece(t, j));
+        } else if (l > 0 && a.pl.bb_shared) {
+          for (int j = 0; j < 3; ++j)
+            store_bf16(imgb + a.pl.off_bb[0], kEncK, n % rows, 3 * (l - 1) + j, bias_piece(t, j));
         } else if (l > 0 && a.pl.off_bb[l]) {
-          uint8_t* img = a.out + a.pl.off_bb[l];
-          for (int j = 0; j < 3; ++j) store_bf16(img, kEncK, n, j, bias_piece(t, j));
+          for (int j = 0; j < 3; ++j) store_bf16(a.out + a.pl.off_bb[l], kEncK, n, j, bias_piece(t, j));
         }
         done = true;
       }

@@ -12,8 +12,16 @@
 
 using namespace nb;
 
+__device__ __forceinline__ bool try_wait_nohint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+static __device__ int g_wait_mode;  // 0: try_wait + hint, 1: try_wait, 2: test_wait spin
+
 template <int NSLOT, int WPS, int G, bool DUMMY_ST, bool CPM = false>
-__global__ void k_chain(int iters, unsigned long long* out) {
+__global__ void k_chain(int iters, unsigned long long* out, int spin) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bars[8];
@@ -39,6 +47,11 @@ __global__ void k_chain(int iters, unsigned long long* out) {
   __syncthreads();
   unsigned long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if (spin > 0) {  // synthetic epilogue latency (ALU-free)
+      const long long t = clock64();
+      while (clock64() - t < spin) {
+      }
+    }
     if (DUMMY_ST) {  // the A-operand stores an epilogue would do (32 columns per row)
       uint32_t r[16];
       for (int j = 0; j < 16; ++j) r[j] = j + it;
@@ -60,7 +73,12 @@ __global__ void k_chain(int iters, unsigned long long* out) {
       }
       __syncwarp();
     }
-    mbar_wait(smem_u32(&bars[s]), ph);
+    {
+      const int wm = g_wait_mode;
+      if (wm == 0) mbar_wait(smem_u32(&bars[s]), ph);
+      else if (wm == 1) while (!try_wait_nohint(smem_u32(&bars[s]), ph)) {}
+      else while (!mbar_test_wait(smem_u32(&bars[s]), ph)) {}
+    }
     ph ^= 1u;
     tc_fence_after();
   }
@@ -79,6 +97,8 @@ static double avg(unsigned long long* d, int n) {
   return (double)s / n;
 }
 
+static int g_spin = 0;
+
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, sizeof(unsigned long long) * 1024);
@@ -87,15 +107,25 @@ int main() {
   {                                                                                               \
     auto k = k_chain<NS, WP, G, ST, ##__VA_ARGS__>;                                                              \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);             \
-    k<<<grid, NS * WP * 32, 120 * 1024>>>(iters, d);                                              \
+    k<<<grid, NS * WP * 32, 120 * 1024>>>(iters, d, g_spin);                                      \
     cudaError_t e = cudaDeviceSynchronize();                                                      \
     double c = avg(d, grid);                                                                      \
-    printf("slots=%d wps=%d G=%d st=%d: %.1f cycles per MMA, %.0f per group-round %s\n", NS, WP, G, \
-           (int)ST, c / ((double)iters * NS * G), c / iters, cudaGetErrorString(e));              \
+    printf("slots=%d wps=%d G=%d st=%d spin=%d: %.1f cycles per MMA, %.0f per group-round %s\n", NS, WP, G, \
+           (int)ST, g_spin, c / ((double)iters * NS * G), c / iters, cudaGetErrorString(e));     \
   }
   RUN(1, 4, 5, false) RUN(2, 4, 5, false) RUN(3, 4, 5, false) RUN(4, 4, 5, false) RUN(5, 4, 5, false)
   RUN(5, 4, 4, false) RUN(5, 4, 1, false) RUN(5, 1, 5, false)
   RUN(5, 4, 5, true) RUN(4, 8, 5, true) RUN(5, 4, 4, true)
+  for (int wm : {0, 1, 2}) {
+    cudaMemcpyToSymbol(g_wait_mode, &wm, sizeof(int));
+    printf("-- wait mode %d\n", wm);
+    for (int sp : {0, 400, 800}) {
+      g_spin = sp;
+      RUN(5, 4, 5, true) RUN(5, 4, 1, true)
+    }
+  }
+  { int wm = 0; cudaMemcpyToSymbol(g_wait_mode, &wm, sizeof(int)); }
+  g_spin = 0;
   printf("-- commit after every MMA:\n");
   RUN(5, 4, 5, false, true) RUN(3, 4, 5, false, true) RUN(5, 1, 5, false, true)
   return 0;
