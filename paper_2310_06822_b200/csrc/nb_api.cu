@@ -115,6 +115,24 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   pl->bytes = align_up(off, 16u);
 }
 
+static void bwd_layout(const nb_desc& d, BwdLayout* bl) {
+  uint32_t off = 0;
+  const uint32_t W = (uint32_t)d.width;
+  for (int l = 0; l < kMaxLayers; ++l) {
+    bl->off_wt[l] = 0;
+    if (l >= 1 && l < d.hidden_layers) {
+      bl->off_wt[l] = off;
+      off = align_up(off + (W / 2) * W * 2u, 128u);
+    }
+  }
+  bl->off_wout = off; off = align_up(off + 4u * W, 16u);
+  for (int k = 0; k < 2; ++k) {
+    bl->off_u[k] = off;
+    off = align_up(off + 4u * W, 16u);
+  }
+  bl->bytes = align_up(off, 128u);
+}
+
 // Report sticky in-kernel flags (and clear them).  Host mirror is pinned.
 static nb_status take_flags(nb_model* m, cudaStream_t s, nb_status ok) {
   unsigned int f = 0;
@@ -258,6 +276,10 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->adam_v, sizeof(float) * m->P);
   A((void**)&m->grad, sizeof(float) * m->P);
   A((void**)&m->packed, (size_t)m->pl.bytes * m->pl.pairs);
+  if (m->pl.pairs == 2) {
+    bwd_layout(m->d, &m->bl);
+    A((void**)&m->packed_bwd, (size_t)m->bl.bytes * 2);
+  }
   A((void**)&m->d_tau, sizeof(float) * 4);
   // kernel counters i * kCtrStride (kept zero between launches by the
   // finalising CTA), finalised totals at kFinOff, a zero block at kZeroOff
@@ -298,6 +320,7 @@ void nb_model_destroy(nb_model* m) {
   cudaFree(m->adam_v);
   cudaFree(m->grad);
   cudaFree(m->packed);
+  cudaFree(m->packed_bwd);
   cudaFree(m->d_tau);
   cudaFree(m->d_counts);
   cudaFree(m->d_keys);

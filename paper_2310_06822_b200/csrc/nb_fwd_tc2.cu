@@ -26,52 +26,6 @@ struct TcParams2 {
   int64_t num_pairs;      // 256-row tile pairs
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, 10000000;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mma_ts2(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit2(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
-
 template <bool ONES>
 __device__ __forceinline__ void encode_cols2(const float* x, int d0, uint32_t (&col)[8]) {
   uint32_t h[8], l[8];
@@ -309,6 +263,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
       uint32_t c[8];
       encode_cols2<BF>(x, d0, c);
       tmem_st8(trow + ACOL, c);
+      if (MODE == kTrain && 2 * t + rank < p.a.tr.num_tiles) {  // layer-1 input image (dW GEMM)
+        uint8_t* base = p.a.tr.x_img + (2 * t + rank) * img_tile_bytes(16);
+#pragma unroll
+        for (int fg = 0; fg < 2; ++fg)
+          *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+              make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+      }
       tmem_wait_st();
     }
     sync_and_issue(0);
@@ -356,11 +317,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
             add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
           }
         }
-        if (!last) {
+        if (!last || MODE == kTrain) {
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
-          tmem_st16(trow + ACOL + (uint32_t)((col0 + 32 * c) / 2), pk);
+          if (!last) tmem_st16(trow + ACOL + (uint32_t)((col0 + 32 * c) / 2), pk);
+          if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image
+            uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
+            const int fg0 = (col0 + 32 * c) / 8;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<uint4*>(base + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                  make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
         }
         if (l == h0 || l == h1 || last) {
 #pragma unroll
@@ -414,6 +383,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
           if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
           if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
         }
+      } else if (MODE == kTrain) {
+        // Eq. (1): w = alpha if y else beta; term w softplus(-+z);
+        // dL/dz = w (sigmoid(z) - y) / B; exit heads add the same term
+        const float yf = (float)ythis;
+        const float w = valid ? (ythis ? p.a.tr.alpha : p.a.tr.beta) : 0.f;
+        auto sp = [](float u) { return fmaxf(u, 0.f) + log1pf(__expf(-fabsf(u))); };
+        float lsum = w * sp(ythis ? -z : z);
+        const float gz = w * (1.f / (1.f + __expf(-z)) - yf) * p.a.tr.inv_b;
+        float ge[2] = {0.f, 0.f};
+        for (int k = 0; k < NH; ++k) {
+          lsum += w * sp(ythis ? -e[k] : e[k]);
+          ge[k] = w * (1.f / (1.f + __expf(-e[k])) - yf) * p.a.tr.inv_b;
+        }
+        if (valid) {
+          p.a.tr.g32[r * 3] = gz;
+          p.a.tr.g32[r * 3 + 1] = ge[0];
+          p.a.tr.g32[r * 3 + 2] = ge[1];
+        }
+        if (2 * tile + rank < p.a.tr.num_tiles) {
+          uint8_t* hb = p.a.tr.hd_img + (2 * tile + rank) * img_tile_bytes(8) + (rit / 8) * 128 +
+                        (rit % 8) * 16;
+          *reinterpret_cast<uint4*>(hb) =
+              make_uint4(pack_bf16x2(gz, ge[0]), pack_bf16x2(ge[1], 0.f), 0u, 0u);
+        }
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xFFFFFFFFu, lsum, o);
+        const bool pred = z >= 0.f, yy = ythis != 0;
+        const uint32_t c0 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
+        const uint32_t c1 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
+        const uint32_t c2 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && yy));
+        const uint32_t c3 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
+        if (lane == 0) {
+          atomicAdd(p.a.tr.loss, (double)lsum * (double)p.a.tr.inv_b);
+          cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
+        }
       } else {
         classify2<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
       }
@@ -421,7 +424,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
     par ^= 1u;
     tile = next;
   }
-  if (lead && MODE != kForward) {
+  if (MODE == kTrain && lead && lane == 0) {
+    for (int i = 0; i < 4; ++i)
+      if (cnt[i]) atomicAdd(p.a.tr.stats + i, (unsigned long long)cnt[i]);
+  }
+  if (lead && MODE != kForward && MODE != kTrain) {
     if (MODE == kCalibrate) {
       for (int k = 0; k <= NH; ++k) {
         const uint32_t mk = __reduce_min_sync(0xFFFFFFFFu, key[k]);
@@ -472,12 +479,12 @@ static cudaError_t launch_tc2_m(const nb_model* m, const FwdArgs& a, cudaStream_
 template <int LC, bool BF>
 static cudaError_t launch_tc2_l(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
   if (mode == kForward) return launch_tc2_m<LC, kForward, BF>(m, a, st);
+  if (mode == kTrain) return launch_tc2_m<LC, kTrain, BF>(m, a, st);
   if (mode == kCalibrate) return launch_tc2_m<LC, kCalibrate, BF>(m, a, st);
   return launch_tc2_m<LC, kScore, BF>(m, a, st);
 }
 
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
-  if (mode == kTrain) return cudaErrorNotSupported;
   const bool bf = m->pl.bias_l0 && m->pl.bb_shared;
   if (m->d.hidden_layers == 4)
     return bf ? launch_tc2_l<4, true>(m, mode, a, st) : launch_tc2_l<4, false>(m, mode, a, st);

@@ -51,6 +51,16 @@ struct PackLayout {
   uint32_t pairs;              // 1, or 2 for CTA-pair widths (2 images, each with W/2 rows)
 };
 
+// Transposed pair images for the w = 256 backward chain (CTA pairs): image v
+// holds, for each hidden layer l >= 1, W_l^T rows = input features
+// [128 v, 128 v + 128) x K = 256 output features (K-major core matrices, the
+// N half of cta_group::2's B), then fp32 w_out and the head vectors.
+struct BwdLayout {
+  uint32_t off_wt[kMaxLayers];  // layer l >= 1
+  uint32_t off_wout, off_u[2];
+  uint32_t bytes;               // one image
+};
+
 struct ParamOffsets {  // canonical fp32 blob offsets (nb.h nb_num_params)
   int64_t W[kMaxLayers], b[kMaxLayers], wout, bout, u[2], c[2];
 };
@@ -71,6 +81,8 @@ struct nb_model {
   float* grad = nullptr;      // [P] gradient of the current step
   int64_t step = 0;
   uint8_t* packed = nullptr;  // bf16 packed image (pl.bytes)
+  nb::BwdLayout bl;
+  uint8_t* packed_bwd = nullptr;  // w = 256 training: 2 transposed pair images (bl.bytes)
   float tau[3] = {0, 0, 0};
   float* d_tau = nullptr;     // [3]
   unsigned long long* d_counts = nullptr;  // counters (strided), totals, zeros: 256 words
@@ -123,6 +135,7 @@ struct TrainArgs {
   float alpha, beta, inv_b;      // Eq. (1) weights, 1 / n_global
   double* loss;
   unsigned long long* stats;     // batch tp fp fn tn at z >= 0
+  int64_t num_tiles;             // 128-row tiles with images (CTA-pair kernel bound)
 };
 
 struct FwdArgs {
@@ -160,6 +173,8 @@ cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                             int64_t n_global, float alpha, float beta, cudaStream_t s);
 bool train_tc_supported(const nb_desc& d);
+cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8_t* const* d_img,
+                           const float* g32, int64_t n, cudaStream_t st);
 size_t train_tc_scratch_bytes(const nb_model* m, int64_t n);
 size_t train_simt_scratch_bytes(const nb_model* m, int64_t n);
 cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s);

@@ -65,6 +65,8 @@ cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* ou
 struct PackArgs {
   const float* theta;
   uint8_t* out;
+  uint8_t* out_bwd;  // transposed pair images (w = 256) or NULL
+  BwdLayout bl;
   PackLayout pl;
   ParamOffsets po;
   int W, L, d0, nh;
@@ -127,6 +129,25 @@ __global__ void k_pack_bf16(PackArgs a) {
           __float2bfloat16_rn(v);
     }
   }
+  // transposed pair images: W_l[o][i] -> image i / 128, row i % 128, column o (K = W)
+  if (a.out_bwd) {
+    for (int l = 1; l < a.L; ++l) {
+      for (int64_t e = tid; e < (int64_t)W * W; e += stride) {
+        const int o = (int)(e / W), i = (int)(e % W);
+        __nv_bfloat16* img = (__nv_bfloat16*)(a.out_bwd + (size_t)(i / rows) * a.bl.bytes + a.bl.off_wt[l]);
+        const int r = i % rows;
+        img[(int64_t)(r / 8) * (W / 8) * 64 + (o / 8) * 64 + (r % 8) * 8 + (o % 8)] =
+            __float2bfloat16_rn(a.theta[a.po.W[l] + e]);
+      }
+    }
+    for (int64_t e = tid; e < (int64_t)W; e += stride) {
+      for (int im = 0; im < 2; ++im) {
+        uint8_t* b = a.out_bwd + (size_t)im * a.bl.bytes;
+        ((float*)(b + a.bl.off_wout))[e] = a.theta[a.po.wout + e];
+        for (int k = 0; k < a.nh; ++k) ((float*)(b + a.bl.off_u[k]))[e] = a.theta[a.po.u[k] + e];
+      }
+    }
+  }
   float* bias = (float*)(a.out + a.pl.off_bias);
   for (int64_t e = tid; e < (int64_t)a.L * W; e += stride)
     bias[e] = a.theta[a.po.b[e / W] + e % W];
@@ -151,6 +172,8 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s) {
   PackArgs a;
   a.theta = m->theta;
   a.out = m->packed;
+  a.out_bwd = m->packed_bwd;
+  a.bl = m->bl;
   a.pl = m->pl;
   a.po = m->po;
   a.W = m->d.width;
@@ -618,6 +641,8 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
         uint8_t* img = a.out + (size_t)(n / rows) * a.pl.bytes + a.pl.off_w[l];
         store_bf16(img, (int)a.pl.k_of[l], n % rows, k, t);
         if (l == 0) store_bf16(img, (int)a.pl.k_of[0], n % rows, a.d0 + k, t);  // lo copy
+        if (l > 0 && a.out_bwd)  // transposed pair image: row = input feature k, column = n
+          store_bf16(a.out_bwd + (size_t)(k / rows) * a.bl.bytes + a.bl.off_wt[l], W, k % rows, n, t);
         done = true;
       } else if (i >= ob && i < ob + W) {
         const int n = (int)(i - ob);
@@ -636,11 +661,23 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
       }
     }
     if (done) continue;
-    if (i >= a.po.wout && i < a.po.wout + W) fp32_tail(a.pl.off_wout + 4u * (uint32_t)(i - a.po.wout));
-    else if (i == a.po.bout) fp32_tail(a.pl.off_bout);
+    auto bwd_tail = [&](uint32_t off_bytes) {
+      if (a.out_bwd)
+        for (int im = 0; im < 2; ++im) *reinterpret_cast<float*>(a.out_bwd + (size_t)im * a.bl.bytes + off_bytes) = t;
+    };
+    if (i >= a.po.wout && i < a.po.wout + W) {
+      fp32_tail(a.pl.off_wout + 4u * (uint32_t)(i - a.po.wout));
+      bwd_tail(a.bl.off_wout + 4u * (uint32_t)(i - a.po.wout));
+    } else if (i == a.po.bout) {
+      fp32_tail(a.pl.off_bout);
+    }
     for (int k = 0; k < a.nh; ++k) {
-      if (i >= a.po.u[k] && i < a.po.u[k] + W) fp32_tail(a.pl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
-      else if (i == a.po.c[k]) fp32_tail(a.pl.off_c + 4u * (uint32_t)k);
+      if (i >= a.po.u[k] && i < a.po.u[k] + W) {
+        fp32_tail(a.pl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
+        bwd_tail(a.bl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
+      } else if (i == a.po.c[k]) {
+        fp32_tail(a.pl.off_c + 4u * (uint32_t)k);
+      }
     }
   }
 }
@@ -652,6 +689,8 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
   PackArgs a;
   a.theta = m->theta;
   a.out = m->packed;
+  a.out_bwd = m->packed_bwd;
+  a.bl = m->bl;
   a.pl = m->pl;
   a.po = m->po;
   a.W = m->d.width;

@@ -216,7 +216,7 @@ struct DwJob {
   float* w_out;
   float* b_out;
 };
-constexpr int kMaxDwJobs = kMaxLayers + 3;
+constexpr int kMaxDwJobs = 2 * kMaxLayers + 3;
 constexpr int kDwCols = kDwMaxN + 16;  // partial columns per CTA (features + ones block)
 // partial of CTA c of job j, column col, D row m: [(j * cpj + c) * kDwCols + col] * 128 + m
 struct DwJobs {
@@ -292,8 +292,9 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
     for (int i = 0; i < (int)ntl; ++i) {
       // NST - 1 tiles in flight: refilling the stage of tile i - 1 (whose MMAs
       // may still run) is left to the next iteration
+      const int ahead = NST >= 3 ? NST - 1 : NST;
       if (lane == 0) {
-        for (; issued < (int)ntl && issued < i + NST - 1; ++issued) {
+        for (; issued < (int)ntl && issued < i + ahead; ++issued) {
           issue_copy(issued, ist, (pround & 1u) ^ 1u);
           if (++ist == NST) {
             ist = 0;
@@ -412,7 +413,8 @@ __global__ void k_dw_reduce(const __grid_constant__ DwJobs js) {
 // host side
 // ---------------------------------------------------------------------------
 bool train_tc_supported(const nb_desc& d) {
-  return d.precision == NB_BF16 && (d.width == 64 || d.width == 128) && d.hidden_layers >= 2;
+  return d.precision == NB_BF16 && (d.width == 64 || d.width == 128 || d.width == 256) &&
+         d.hidden_layers >= 2;
 }
 
 struct TrainLayout {
@@ -475,6 +477,7 @@ static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
 }
 
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
 
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                             int64_t n_global, float alpha, float beta, cudaStream_t st) {
@@ -501,8 +504,10 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   a.tr.inv_b = 1.0f / (float)n_global;
   a.tr.loss = m->d_loss;
   a.tr.stats = m->d_stats;
+  a.tr.num_tiles = T;
+  const bool pairs = m->pl.pairs == 2;  // w = 256: CTA-pair forward and backward
   cudaError_t e = cudaSuccess;
-  if (n > 0) e = launch_fwd_tc(m, kTrain, a, st);
+  if (n > 0) e = pairs ? launch_fwd_tc2(m, kTrain, a, st) : launch_fwd_tc(m, kTrain, a, st);
   if (e != cudaSuccess) return e;
   // 2. backward chain
   BwdParams bp;
@@ -519,7 +524,10 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     bp.d_img[l] = base + tl.d_img[l];
   }
   bp.g32 = (float*)(base + tl.g32);
-  if (n > 0) e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
+  if (n > 0 && pairs)
+    e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st);
+  else if (n > 0)
+    e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
   if (e != cudaSuccess) return e;
   // 3 + 4. dW GEMM jobs (one launch) and their deterministic reduction (one launch)
   DwJobs js{};
@@ -527,8 +535,11 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   float* g = m->grad;
   auto add = [&](const uint8_t* a_img, int fa, const uint8_t* b_img, int fb, int kind, int rows,
                  int row, int in, float* w_out, float* b_out) {
-    DwJob& j = js.job[js.njobs++];
-    j = DwJob{a_img, fa, 0, b_img, fb, kind, rows, row, d0, in, w_out, b_out};
+    // A with more than 128 features (w = 256): one job per 128-feature M half
+    for (int mo = 0; mo < fa; mo += 128) {
+      DwJob& j = js.job[js.njobs++];
+      j = DwJob{a_img, fa, mo, b_img, fb, kind, std::min(rows, 128), row, d0, in, w_out, b_out};
+    }
   };
   for (int l = 0; l < L; ++l) {
     if (l == 0)

@@ -259,7 +259,8 @@ def param_tensors(cfg):
     return out
 
 
-@pytest.mark.parametrize("name,n", [("c2", (1 << 13) + 77), ("c3", (1 << 12) + 5), ("c4", (1 << 12) + 33)])
+@pytest.mark.parametrize("name,n", [("c2", (1 << 13) + 77), ("c3", (1 << 12) + 5), ("c4", (1 << 12) + 33),
+                                    ("c5", (1 << 12) + 300)])
 def test_bf16_train_step_gradient_parity(name, n):
     """P3: one step from identical state, per parameter tensor
     ||g_gpu - g_oracle|| <= 2e-2 ||g_oracle|| (BASELINE.json north_star)."""
@@ -391,7 +392,7 @@ def test_score_async_matches_score():
         m.score_async(q, y, torch.zeros(9, dtype=torch.int64))
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_fused_adam_repack_matches_full_pack(name):
     """The training step's fused Adam + bf16 re-pack leaves exactly the image a
     full pack of the updated fp32 master builds: logits after 3 steps equal the
