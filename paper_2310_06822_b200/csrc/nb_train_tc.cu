@@ -223,6 +223,7 @@ struct DwJobs {
   DwJob job[kMaxDwJobs];
   int njobs, cpj;
   int nst;        // TMA pipeline stages (<= kDwMaxStages)
+  int accumulate; // add into the partials (micro-batches after the first)
   uint32_t stage; // bytes per stage (A 32 KB + B of the widest job + ones block)
   float* partial;
 };
@@ -344,7 +345,10 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
       tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) out[(int64_t)(c + i) * 128] = t1 > t0 ? __uint_as_float(v[i]) : 0.f;
+      for (int i = 0; i < 32; ++i) {
+        const float x = t1 > t0 ? __uint_as_float(v[i]) : 0.f;
+        out[(int64_t)(c + i) * 128] = js.accumulate ? out[(int64_t)(c + i) * 128] + x : x;
+      }
       c += 16;
     } else {
       uint32_t w[16];
@@ -357,7 +361,10 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
           : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c));
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) out[(int64_t)(c + i) * 128] = t1 > t0 ? __uint_as_float(w[i]) : 0.f;
+      for (int i = 0; i < 16; ++i) {
+        const float x = t1 > t0 ? __uint_as_float(w[i]) : 0.f;
+        out[(int64_t)(c + i) * 128] = js.accumulate ? out[(int64_t)(c + i) * 128] + x : x;
+      }
     }
   }
   tc_fence_before();
@@ -443,8 +450,10 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
   return t;
 }
 
+static int64_t train_chunk_rows(const nb_model* m, int64_t n);
+
 size_t train_tc_scratch_bytes(const nb_model* m, int64_t n) {
-  return train_layout(m, n, m->num_sms).total;
+  return train_layout(m, train_chunk_rows(m, n), m->num_sms).total;
 }
 
 template <int W>
@@ -463,28 +472,39 @@ static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
   for (int i = 0; i < js.njobs; ++i) fbmax = std::max(fbmax, js.job[i].fb);
   js.stage = (uint32_t)(128 * 256 + (fbmax + 16) * 256);
   const size_t fixed = 8 * 2 * kDwMaxStages + 16;
-  js.nst = (int)std::min<size_t>(kDwMaxStages, (227 * 1024 - fixed) / js.stage);  // >= 3
+  js.nst = (int)std::min<size_t>(kDwMaxStages, (227 * 1024 - fixed) / js.stage);
   if (const char* ev = getenv("NB_DW_STAGES"))  // measurement override
     js.nst = std::max(2, std::min(js.nst, atoi(ev)));
   const size_t smem = (size_t)js.nst * js.stage + fixed;
   cudaError_t e = cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_dw_tc<<<dim3(js.cpj, js.njobs), 128, smem, st>>>(js, T);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_dw_reduce<<<64, 256, 0, st>>>(js);
   return cudaGetLastError();
+}
+
+// Rows per training micro-batch: bounds the scratch (activation / delta
+// images, ~2 GB) for very large local batches; dW partials accumulate across
+// micro-batches in a fixed order (deterministic), and one reduce follows the
+// last.  (L2-sized micro-batches of ~64 MB were measured slower: the kernels
+// are latency-bound below ~2^16 rows, e.g. c5 2^18 rows 0.74 -> 2.9 ms.)
+static int64_t train_chunk_rows(const nb_model* m, int64_t n) {
+  const int64_t per_row = 2 * (16 + 2 * (int64_t)m->d.hidden_layers * m->d.width + 8) + 12;
+  int64_t c = ((int64_t)2 << 30) / per_row;
+  if (const char* ev = getenv("NB_TRAIN_CHUNK")) c = atoll(ev);  // test / measurement override
+  c = std::max<int64_t>(256, c / 256 * 256);
+  return std::max<int64_t>(1, std::min(n, c));
 }
 
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
 
-cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
-                            int64_t n_global, float alpha, float beta, cudaStream_t st) {
-  const int W = m->d.width, L = m->d.hidden_layers, d0 = m->d0;
+// One micro-batch: forward (kTrain) + backward chain + dW GEMMs (partials
+// written when `first`, accumulated otherwise).
+static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                               int64_t n_global, float alpha, float beta, bool first,
+                               DwJobs& js, const TrainLayout& tl, cudaStream_t st) {
+  const int W = m->d.width, L = m->d.hidden_layers;
   const int64_t T = (n + kTile - 1) / kTile;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(T, m->num_sms));
-  TrainLayout tl = train_layout(m, n, m->num_sms);
   uint8_t* base = (uint8_t*)m->train_scratch;
   // 1. forward with activation images and dL/dz
   FwdArgs a;
@@ -506,8 +526,7 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   a.tr.stats = m->d_stats;
   a.tr.num_tiles = T;
   const bool pairs = m->pl.pairs == 2;  // w = 256: CTA-pair forward and backward
-  cudaError_t e = cudaSuccess;
-  if (n > 0) e = pairs ? launch_fwd_tc2(m, kTrain, a, st) : launch_fwd_tc(m, kTrain, a, st);
+  cudaError_t e = pairs ? launch_fwd_tc2(m, kTrain, a, st) : launch_fwd_tc(m, kTrain, a, st);
   if (e != cudaSuccess) return e;
   // 2. backward chain
   BwdParams bp;
@@ -524,12 +543,23 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     bp.d_img[l] = base + tl.d_img[l];
   }
   bp.g32 = (float*)(base + tl.g32);
-  if (n > 0 && pairs)
+  if (pairs)
     e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st);
-  else if (n > 0)
+  else
     e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
   if (e != cudaSuccess) return e;
-  // 3 + 4. dW GEMM jobs (one launch) and their deterministic reduction (one launch)
+  // 3. dW GEMMs of every job (one launch)
+  js.accumulate = first ? 0 : 1;
+  return run_dw(js, T, st);
+}
+
+cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                            int64_t n_global, float alpha, float beta, cudaStream_t st) {
+  const int W = m->d.width, L = m->d.hidden_layers, d0 = m->d0;
+  const int64_t chunk = train_chunk_rows(m, n);
+  TrainLayout tl = train_layout(m, chunk, m->num_sms);
+  uint8_t* base = (uint8_t*)m->train_scratch;
+  // dW jobs (image pointers are the same for every micro-batch)
   DwJobs js{};
   js.partial = (float*)(base + tl.partial);
   float* g = m->grad;
@@ -552,19 +582,20 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   for (int k = 0; k < m->d.n_heads; ++k)
     add(base + tl.hd_img, 8, base + tl.h_img[m->d.head_after[k] - 1], W, 2, 1, 1 + k, W,
         g + m->po.u[k], g + m->po.c[k]);
-  js.cpj = (int)std::max<int64_t>(1, std::min<int64_t>(T, m->num_sms / js.njobs));
-  if (e == cudaSuccess) {
-    if (n > 0) {
-      e = run_dw(js, T, st);
-    } else {  // empty batch: zero gradient
-      e = cudaMemsetAsync(js.partial, 0, sizeof(float) * 128 * kDwCols * js.cpj * js.njobs, st);
-      if (e == cudaSuccess) {
-        k_dw_reduce<<<64, 256, 0, st>>>(js);
-        e = cudaGetLastError();
-      }
-    }
+  // a fixed CTA grid per job, the same for every micro-batch (deterministic sums)
+  js.cpj = std::max(1, m->num_sms / js.njobs);
+  cudaError_t e = cudaSuccess;
+  if (n == 0) {  // empty batch: zero gradient
+    e = cudaMemsetAsync(js.partial, 0, sizeof(float) * 128 * kDwCols * js.cpj * js.njobs, st);
   }
-  return e;
+  for (int64_t c0 = 0; c0 < n && e == cudaSuccess; c0 += chunk) {
+    const int64_t rows = std::min(chunk, n - c0);
+    e = train_chunk(m, q + c0 * d0, y + c0, rows, n_global, alpha, beta, c0 == 0, js, tl, st);
+  }
+  if (e != cudaSuccess) return e;
+  // 4. fixed-order reduction of all partials into the gradient blob
+  k_dw_reduce<<<64, 256, 0, st>>>(js);
+  return cudaGetLastError();
 }
 
 }  // namespace nb

@@ -410,3 +410,28 @@ def test_fused_adam_repack_matches_full_pack(name):
     m2.set_params(th)
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 128 * 40 + 3, device=f"cuda:{DEV}")
     assert torch.equal(m.forward(q), m2.forward(q))
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_train_micro_batches_equal_one_batch(name, monkeypatch):
+    """A step split into micro-batches (dW partials accumulated in a fixed order)
+    gives the single-batch gradient up to fp32 summation order, and the same
+    loss and batch counts."""
+    cfg = nbgen.CONFIGS[name]
+    n = 5 * 1024 + 77
+    q = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 9)
+    out = []
+    for chunk in (None, "1024"):
+        if chunk:
+            monkeypatch.setenv("NB_TRAIN_CHUNK", chunk)
+        m = nb.Model(desc_of(cfg), DEV)
+        m.set_params(th)
+        st = m.train_step(cuda(q), cuda(y), alpha=20.0, beta=1.0, lr=1e-3, stats=True)
+        out.append((st, m.get_grad().double().numpy()))
+        monkeypatch.delenv("NB_TRAIN_CHUNK", raising=False)
+    (s1, g1), (s2, g2) = out
+    assert all(s1[k] == s2[k] for k in ("tp", "fp", "fn", "tn"))
+    assert abs(s1["loss"] - s2["loss"]) <= 1e-5 * abs(s1["loss"])
+    assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g1)
