@@ -32,8 +32,22 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = "c2"
-N_PER_RANK = 1 << 22
+CONFIG = "c2"  # --config: c2 (default, BASELINE.json configs[1]) .. c5
+# Queries per step (BASELINE.json): c2 2^22, c3 2^24, c4 2^26 per rank (weak
+# scaling); c5 2^28 in total, sharded over the ranks (strong scaling, BJ.c5).
+N_STEP = {"c2": 1 << 22, "c3": 1 << 24, "c4": 1 << 26, "c5": 1 << 28}
+STRONG = {"c5"}
+WORKLOAD = {
+    "c2": "BASELINE.json configs[1], 3D point bounding, 3->64x4->1 ReLU bf16 (fp32 accumulate), "
+          "2^22 uniform points per rank per step",
+    "c3": "BASELINE.json configs[2], 3D ray bounding, 6->128x4->1 ReLU bf16, 2^24 rays per rank per step",
+    "c4": "BASELINE.json configs[3], 4D animated point bounding, 4->128x6->1 ReLU bf16 with exit heads "
+          "after hidden 2 and 4, 2^26 queries per rank per step",
+    "c5": "BASELINE.json configs[4], 3D box bounding, 6->256x4->1 ReLU bf16 on CTA pairs, 2^28 boxes "
+          "per step sharded over the ranks",
+}
+KERNEL = {"c2": "k_fwd_tc<64,4,0,0,kScore,d0=3,BF>", "c3": "k_fwd_tc<128,4,0,0,kScore,d0=6,BF>",
+          "c4": "k_fwd_tc<128,6,2,4,kScore,d0=4,BF>", "c5": "k_fwd_tc2<4,kScore,BF> (CTA pairs)"}
 METRIC = "bounding queries/s"
 UNIT = "queries/s"
 
@@ -59,7 +73,7 @@ def load_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        k = d.get(CONFIG, {}).get("score_kernel", {})
+        k = d.get(CONFIG, {}).get("score_kernel", {})  # (only for the captured config)
         if "dram_bytes_per_launch" in k:
             return k["dram_bytes_per_launch"], k.get("tensor_pipe_pct")
     return None, None
@@ -153,7 +167,8 @@ def run_reference(args):
     th = (nbgen.init_params(cfg) * 2.5).double().numpy()
     n = args.ref_sample
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n).numpy()
-    y = oracle.label(grid, 3, "point", q)
+    frames = grid.shape[0] if cfg.space_dim == 4 else 1
+    y = oracle.label(grid, cfg.space_dim, cfg.kind, q, frames=frames)
     z = oracle.forward(a, th, q)  # warm, and the calibration pass
     tau, _ = oracle.calibrate(z, y)
     for _ in range(args.warmup if args.warmup < 2 else 1):
@@ -171,10 +186,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{CONFIG}: 3D point bounding, 3->64x4->1, oracle sample of {n} "
-                               f"points per step (full step is 2^22)", "global_batch": n},
+        "config": {"workload": f"{CONFIG}: {WORKLOAD[CONFIG]}; oracle sample of {n} queries per step",
+                   "global_batch": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{n} c2 EVAL points, fp64 forward + calibrated score"},
+                         "sample": f"{n} {CONFIG} EVAL queries, fp64 forward + calibrated score"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0, "counts_sample": {k: c[k] for k in ("tp", "fp", "fn", "tn")},
     }
@@ -191,14 +206,16 @@ def cpu_baseline_sample(n=1 << 18):
     a = oracle.arch_of(cfg)
     th = (nbgen.init_params(cfg) * 2.5).double().numpy()
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n).numpy()
-    y = oracle.label(nbgen.make_grid(cfg).numpy(), 3, "point", q)
+    grid = nbgen.make_grid(cfg).numpy()
+    frames = grid.shape[0] if cfg.space_dim == 4 else 1
+    y = oracle.label(grid, cfg.space_dim, cfg.kind, q, frames=frames)
     t0 = time.perf_counter()
     z = oracle.forward(a, th, q)
     tau, _ = oracle.calibrate(z, y)
     oracle.score(z, y, tau)
     t = time.perf_counter() - t0
     return {"value": n / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{n} c2 EVAL points: fp64 forward + calibrate + score ({t:.1f} s)"}
+            "sample": f"{n} {CONFIG} EVAL queries: fp64 forward + calibrate + score ({t:.1f} s)"}
 
 
 def run_ours(args):
@@ -214,19 +231,21 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = nbgen.CONFIGS[CONFIG]
-    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
+    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
+                   cfg.precision)
     m = nb.Model(desc, local)
     if world > 1:
         from paper_2310_06822_b200.dist import comm_init
 
         comm_init(m)
     m.set_params(nbgen.init_params(cfg) * 2.5)
-    n = N_PER_RANK
+    strong = CONFIG in STRONG
+    n = N_STEP[CONFIG] // world if strong else N_STEP[CONFIG]
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
     grid = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
     y = grid.label(cfg.kind, q)
     tau = m.calibrate(q, y)                       # global tau (allreduce min across ranks)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > the 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
     # one step = nb_score_async: fused encode/MLP/classify/count kernel, NCCL
@@ -304,16 +323,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{CONFIG}: BASELINE.json configs[1], 3D point bounding, "
-                                   "3->64x4->1 ReLU bf16 (fp32 accumulate), 2^22 uniform points per "
-                                   "rank per step, fused forward+calibrated score+counts",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{CONFIG}: {WORKLOAD[CONFIG]}, fused forward+calibrated score+counts",
                        "global_batch": n * world, "per_rank_batch": n,
                        "parallelism": f"dp{world} (query shards, NCCL allreduce of counts)",
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_fwd_tc<64,4,0,0,kScore>", "flop_per_query": fq,
+                         "kernel": KERNEL[CONFIG], "flop_per_query": fq,
                          "kernel_ms_per_launch": per_launch_ms,
                          "ncu_tensor_pipe_pct": tensor_pct},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (4 * cfg.record_floats + 1),
@@ -342,7 +360,8 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
     import torch
     import torch.distributed as dist
 
-    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, (), cfg.precision)
+    desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
+                   cfg.precision)
     m = nb.Model(desc, local)
     if world > 1:
         from paper_2310_06822_b200.dist import comm_init
@@ -372,7 +391,8 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
     ms = ms.item()
     flop = 3 * flop_per_query(cfg)  # forward + delta back-propagation + dW (algorithmic)
     return {"metric": "train samples/s", "value": B * steps / (ms * 1e-3), "unit": "samples/s",
-            "config": f"{CONFIG} bf16 3->64x4->1, global batch {B}, Adam lr 1e-3, alpha ramp",
+            "config": f"{CONFIG} bf16 {cfg.record_floats}->{cfg.width}x{cfg.hidden_layers}->1, global batch {B}, "
+                      "Adam lr 1e-3, alpha ramp",
             "steps": steps, "ms_per_step": ms / steps,
             "tflops_algorithmic": flop * B * steps / (ms * 1e-3) / 1e12}
 
@@ -383,11 +403,14 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--ref-sample", type=int, default=1 << 20)
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--train-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    global CONFIG
+    CONFIG = args.config
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
