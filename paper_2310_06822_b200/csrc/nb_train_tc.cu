@@ -397,11 +397,24 @@ __global__ void k_dw_reduce(const __grid_constant__ DwJobs js) {
       const int c0 = k == r.in ? r.fb : k;
       const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : -1;
       const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
+      const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
       float acc = 0.f;
-      for (int c = 0; c < js.cpj; ++c) {
-        const float* Pc = P + (int64_t)c * kDwCols * 128;
-        acc += Pc[(int64_t)c0 * 128];
-        if (c1 >= 0) acc += Pc[(int64_t)c1 * 128];
+      // loads of 8 CTAs in flight, summed in CTA order (deterministic)
+      for (int c = 0; c < js.cpj; c += 8) {
+        float x0[8], x1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = c + u < js.cpj;
+          x0[u] = ok ? __ldg(P + (c + u) * cs + (int64_t)c0 * 128) : 0.f;
+          x1[u] = (ok && c1 >= 0) ? __ldg(P + (c + u) * cs + (int64_t)c1 * 128) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (c + u < js.cpj) {
+            acc += x0[u];
+            if (c1 >= 0) acc += x1[u];
+          }
+        }
       }
       if (r.kind == 2) {
         if (k == r.in) *r.b_out = acc;
