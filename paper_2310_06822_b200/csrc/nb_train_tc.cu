@@ -458,7 +458,9 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
   take(img_tile_bytes(128));
   t.hd_img = take(T * img_tile_bytes(8) + img_tile_bytes(128));
   t.g32 = take((size_t)T * kTile * 3 * sizeof(float));
-  t.partial = take((size_t)grid * 128 * kDwCols * sizeof(float));  // njobs * cpj <= grid
+  // njobs * cpj <= grid for the unfused path; the fused kernel (w = 64) keeps
+  // one partial per CTA per job: (L + 1) * grid
+  t.partial = take((size_t)(L + 1) * grid * 128 * kDwCols * sizeof(float));
   t.total = off;
   return t;
 }
@@ -510,6 +512,10 @@ static int64_t train_chunk_rows(const nb_model* m, int64_t n) {
 
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
+bool train_fused_supported(const nb_model* m);
+cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                               int64_t n_global, float alpha, float beta, float* partial,
+                               int* cpj, cudaStream_t st);
 
 // One micro-batch: forward (kTrain) + backward chain + dW GEMMs (partials
 // written when `first`, accumulated otherwise).
@@ -572,6 +578,21 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   const int64_t chunk = train_chunk_rows(m, n);
   TrainLayout tl = train_layout(m, chunk, m->num_sms);
   uint8_t* base = (uint8_t*)m->train_scratch;
+  if (n > 0 && n <= chunk && train_fused_supported(m) && !getenv("NB_NO_FUSED")) {
+    // w = 64: forward + loss + backward + dW in one kernel (nb_train_fused.cu)
+    DwJobs fj{};
+    fj.partial = (float*)(base + tl.partial);
+    float* g = m->grad;
+    fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, 16, 1, W, 0, d0, d0, g + m->po.W[0], g + m->po.b[0]};
+    for (int l = 1; l < L; ++l)
+      fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 0, W, 0, d0, W, g + m->po.W[l], g + m->po.b[l]};
+    // the head gradient rides in row 64 of the last layer's delta image
+    fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
+    cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, st);
+    if (e != cudaSuccess) return e;
+    k_dw_reduce<<<64, 256, 0, st>>>(fj);
+    return cudaGetLastError();
+  }
   // dW jobs (image pointers are the same for every micro-batch)
   DwJobs js{};
   js.partial = (float*)(base + tl.partial);
