@@ -50,8 +50,9 @@ __device__ __forceinline__ uint32_t dw_col(int job, int L) {
   return job == 0 ? 128u : (job <= L - 1 ? 160u + 80u * (uint32_t)(job - 1) : 400u);
 }
 
+// 8 warps: warp w owns TMEM lane quarter w % 4 (rows) and column half w / 4.
 template <int LC>
-__global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
+__global__ void __launch_bounds__(256, 1) k_train_fused(const FusedParams p) {
   constexpr int W = kFusedW;
   const int L = LC ? LC : p.L;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -66,8 +67,10 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
   const uint32_t d_bytes = 128u * 256u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_d + d_bytes);  // [0] w [1] acc [2] dw
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  float* xz = reinterpret_cast<float*>(tmem_slot + 4);  // [128] head partial of half 1, then dz
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rit = threadIdx.x;  // row of the tile (lane quarter = warp)
+  const int qw = warp & 3, hf = warp >> 2, col0 = 32 * hf;
+  const int rit = qw * 32 + lane;  // row of the tile (lane quarter qw)
   const uint32_t w_bar = smem_u32(bars), acc_bar = smem_u32(bars + 1), dw_bar = smem_u32(bars + 2);
   if (warp == 0) {
     if (lane == 0) {
@@ -107,9 +110,9 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
   tc_fence_after();
   mbar_wait(w_bar, 0);
 
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
   const uint32_t DCOL = 0, ACOL = 64, ONES = 96;
-  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout);
+  const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
   const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
   const uint32_t idesc_f = make_idesc_bf16(128, W);          // forward: A TMEM (K-major), B K-major
   const uint32_t idesc_b = make_idesc_bf16(128, W, 0, 1);    // backward: B = W_l read MN-major
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
   uint32_t lcnt[4] = {0u, 0u, 0u, 0u};
   double lsum_all = 0.0;
 
-  auto sync = [&]() {  // all 4 warps: TMEM stores and smem image writes done
+  auto sync = [&]() {  // all warps: TMEM stores and smem image writes done
     tc_fence_before();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -147,50 +150,50 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
   for (int64_t tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
     const int64_t r = tile * kTile + rit;
     const bool valid = r < p.n;
-    float x[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = (valid && j < d0) ? __ldg(p.q + r * d0 + j) : 0.f;
-    const int yv = valid ? (int)__ldg(p.y + r) : 0;
-    uint32_t c[8];
-    encode_cols<0, true>(x, d0, c);
+    int yv = 0;
     // the previous tile's dW job 0 reads the x image: wait for it
     if (!first) {
       mbar_wait(dw_bar, dph);
       dph ^= 1u;
     }
-    tmem_st8(trow + ACOL, c);
-    {  // x image features 0..15 (the encoded operand incl. the bias ones; the
-       // dW reduce reads only the hi/lo columns and the ones block at 16)
+    if (hf == 0) {
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = (valid && j < d0) ? __ldg(p.q + r * d0 + j) : 0.f;
+      yv = valid ? (int)__ldg(p.y + r) : 0;
+      uint32_t c[8];
+      encode_cols<0, true>(x, d0, c);
+      tmem_st8(trow + ACOL, c);
+      // x image features 0..15 (the encoded operand incl. the bias ones; the dW
+      // reduce reads only the hi/lo columns and the ones block at 16)
 #pragma unroll
       for (int fg = 0; fg < 2; ++fg)
         *reinterpret_cast<uint4*>(smem + off_x + fimg(rit, fg)) =
             make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+      tmem_wait_st();
     }
-    tmem_wait_st();
     sync();
     issue([&] {
       mma_ts(tmem + DCOL, tmem + ACOL, wdesc(0), idesc_f, 0u);
       mma_commit(acc_bar);
     });
     // ---------------- forward ----------------
-    float z = bout;
+    float zpart = 0.f;
     for (int l = 0; l < L; ++l) {
       wait_acc();
-      uint32_t v[64];
-      tmem_ld32(trow + DCOL, *reinterpret_cast<uint32_t(*)[32]>(v));
-      tmem_ld32(trow + DCOL + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      uint32_t v[32];
+      tmem_ld32(trow + DCOL + (uint32_t)col0, v);
       tmem_wait_ld();
-      uint32_t pk[32];
+      uint32_t pk[16];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) pk[j] = pack_relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+      for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
       // h_l image (MN-major) for the backward masks and the dW GEMMs
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
-        *reinterpret_cast<uint4*>(smem + off_h + l * h_bytes + fimg(rit, g)) =
+      for (int g = 0; g < 4; ++g)
+        *reinterpret_cast<uint4*>(smem + off_h + l * h_bytes + fimg(rit, col0 / 8 + g)) =
             make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
       if (l < L - 1) {
-        tmem_st16(trow + ACOL, *reinterpret_cast<uint32_t(*)[16]>(pk));
-        tmem_st16(trow + ACOL + 16u, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+        tmem_st16(trow + ACOL + (uint32_t)(col0 / 2), pk);
         tmem_wait_st();
         sync();
         issue([&] {
@@ -202,23 +205,27 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
           mma_commit(acc_bar);
         });
       } else {
-        // output head in fp32 (R33): z = w_out . relu(z_L) + b_out
+        // output head in fp32 (R33): z = w_out . relu(z_L) + b_out, two column halves
         float za = 0.f, zb = 0.f;
 #pragma unroll
-        for (int j = 0; j < 64; j += 2) {
+        for (int j = 0; j < 32; j += 2) {
           za = fmaf(fmaxf(__uint_as_float(v[j]), 0.f), wout[j], za);
           zb = fmaf(fmaxf(__uint_as_float(v[j + 1]), 0.f), wout[j + 1], zb);
         }
-        z += za + zb;
+        zpart = za + zb;
       }
     }
     // ---------------- loss (Eq. 1) ----------------
-    const float yf = (float)yv;
-    const float wgt = valid ? (yv ? p.alpha : p.beta) : 0.f;
-    const float sp = fmaxf(yv ? -z : z, 0.f) + log1pf(__expf(-fabsf(z)));
-    lsum_all += (double)(wgt * sp);
-    const float dz = wgt * (1.f / (1.f + __expf(-z)) - yf) * p.inv_b;
-    {
+    if (hf == 1) xz[rit] = zpart;
+    __syncthreads();
+    float dz = 0.f;
+    if (hf == 0) {
+      const float z = bout + (zpart + xz[rit]);
+      const float yf = (float)yv;
+      const float wgt = valid ? (yv ? p.alpha : p.beta) : 0.f;
+      const float sp = fmaxf(yv ? -z : z, 0.f) + log1pf(__expf(-fabsf(z)));
+      lsum_all += (double)(wgt * sp);
+      dz = wgt * (1.f / (1.f + __expf(-z)) - yf) * p.inv_b;
       const bool pred = z >= 0.f, yy = yv != 0;
       lcnt[0] += __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
       lcnt[1] += __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
@@ -226,21 +233,24 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
       lcnt[3] += __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
       if (valid && yv > 1) atomicOr(p.flags, kFlagLabel);
     }
+    __syncthreads();
+    if (hf == 0) xz[rit] = dz;
+    __syncthreads();
+    if (hf == 1) dz = xz[rit];
     // ---------------- backward + dW ----------------
     for (int l = L - 1; l >= 0; --l) {
-      uint32_t v[64];
+      uint32_t v[32];
       if (l < L - 1) {
         wait_acc();  // g_l = delta_{l+1} W_{l+1} (and job l+1's dW MMAs before it)
-        tmem_ld32(trow + DCOL, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld32(trow + DCOL + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld32(trow + DCOL + (uint32_t)col0, v);
         tmem_wait_ld();
       }
       // delta_l = g_l * [h_l > 0], rounded to bf16; written to the delta image
       // (features 0..63; feature 64 = dz for the head job on the last layer)
-      uint32_t pk[32];
+      uint32_t pk[16];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const uint4 hv = *reinterpret_cast<const uint4*>(smem + off_h + l * h_bytes + fimg(rit, g));
+      for (int g = 0; g < 4; ++g) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(smem + off_h + l * h_bytes + fimg(rit, col0 / 8 + g));
         const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -251,16 +261,15 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
         }
       }
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
-        *reinterpret_cast<uint4*>(smem + off_d + fimg(rit, g)) =
+      for (int g = 0; g < 4; ++g)
+        *reinterpret_cast<uint4*>(smem + off_d + fimg(rit, col0 / 8 + g)) =
             make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-      if (l == L - 1)  // dz in feature 64 (feature group 8, element 0)
+      if (hf == 0 && l == L - 1)  // dz in feature 64 (feature group 8, element 0)
         *reinterpret_cast<uint4*>(smem + off_d + fimg(rit, 8)) = make_uint4(pack_bf16x2(dz, 0.f), 0u, 0u, 0u);
-      else if (l == L - 2)  // clear it again for the other layers' rows >= 64 (ignored anyway)
+      else if (hf == 0 && l == L - 2)  // cleared again (rows >= 64 of the other jobs are ignored)
         *reinterpret_cast<uint4*>(smem + off_d + fimg(rit, 8)) = make_uint4(0u, 0u, 0u, 0u);
       if (l >= 1) {
-        tmem_st16(trow + ACOL, *reinterpret_cast<uint32_t(*)[16]>(pk));
-        tmem_st16(trow + ACOL + 16u, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+        tmem_st16(trow + ACOL + (uint32_t)(col0 / 2), pk);
         tmem_wait_st();
       }
       sync();
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
     mbar_wait(dw_bar, dph);
     tc_fence_after();
   }
-  if (lane == 0) {
+  if (hf == 0 && lane == 0) {
     for (int i = 0; i < 4; ++i)
       if (lcnt[i]) atomicAdd(p.stats + i, (unsigned long long)lcnt[i]);
   }
@@ -309,7 +318,7 @@ __global__ void __launch_bounds__(128, 1) k_train_fused(const FusedParams p) {
   if (lane == 0 && ls != 0.0) atomicAdd(p.loss, ls * (double)p.inv_b);
   // dW accumulators -> partials (D row = thread row, column-major, coalesced)
   const int njobs = L + 1;
-  for (int job = 0; job < njobs; ++job) {
+  for (int job = 0; job < njobs && hf == 0; ++job) {
     const int N = job == 0 ? 32 : 80;
     float* out = p.partial + ((int64_t)(job * gridDim.x + blockIdx.x) * kDwColsF) * 128 + rit;
     for (int c0 = 0; c0 < N; c0 += 16) {
@@ -342,7 +351,7 @@ bool train_fused_supported(const nb_model* m) {
 
 size_t train_fused_smem(const nb_model* m) {
   const size_t off_x = (m->pl.bytes + 1023u) & ~(size_t)1023u;
-  return off_x + 32 * 256 + 4 * 80 * 256 + 128 * 256 + 64;
+  return off_x + 32 * 256 + 4 * 80 * 256 + 128 * 256 + 64 + 128 * 4;
 }
 
 cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
@@ -370,7 +379,7 @@ cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, in
   auto kern = p.L == 4 ? k_train_fused<4> : k_train_fused<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, 128, smem, st>>>(p);
+  kern<<<grid, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 

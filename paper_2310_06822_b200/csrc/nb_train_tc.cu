@@ -381,52 +381,79 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
 //   kind 0: hidden layer l >= 2: W[m][k] <- D[m][k], b[m] <- D[m][fb]
 //   kind 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
 //   kind 2: head row `row` of the head-gradient image: v[j] <- D[row][j], c <- D[row][fb]
-__global__ void k_dw_reduce(const __grid_constant__ DwJobs js) {
-  int64_t base = 0;
-  for (int jj = 0; jj < js.njobs; ++jj) {
+// Block = 32 consecutive output elements x 8 slices of the CTA range: thread
+// (e, s) sums CTAs [s * per, (s + 1) * per) in order, then slice 0 adds the 8
+// slice sums in order — a fixed tree, so the result is deterministic.
+constexpr int kRedSlices = 8;
+__global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_constant__ DwJobs js) {
+  __shared__ float part[kRedSlices][32];
+  const int e_in = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  int64_t e = (int64_t)blockIdx.x * 32 + e_in;  // global element index over all jobs
+  int jj = 0;
+  int64_t total = 0;
+  for (; jj < js.njobs; ++jj) {
     const DwJob& r = js.job[jj];
-    const int per_row = r.in + 1;
+    total = (int64_t)(r.kind == 2 ? 1 : r.rows) * (r.in + 1);
+    if (e < total) break;
+    e -= total;
+  }
+  const bool active = jj < js.njobs;
+  float acc = 0.f;
+  int k = 0, m = 0;
+  if (active) {
+    const DwJob& r = js.job[jj];
     const int rows = r.kind == 2 ? 1 : r.rows;
-    const int64_t total = (int64_t)rows * per_row;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - base; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      if (i < 0) continue;
-      const int k = (int)(i / rows);            // output column (k == in: bias)
-      const int mi = (int)(i % rows);
-      const int m = r.kind == 2 ? r.row : mi;   // row of D
-      const int c0 = k == r.in ? r.fb : k;
-      const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : -1;
-      const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
-      const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
-      float acc = 0.f;
-      // loads of 8 CTAs in flight, summed in CTA order (deterministic)
-      for (int c = 0; c < js.cpj; c += 8) {
-        float x0[8], x1[8];
+    k = (int)(e / rows);                          // output column (k == in: bias)
+    m = r.kind == 2 ? r.row : (int)(e % rows);    // row of D
+    const int c0 = k == r.in ? r.fb : k;
+    const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : -1;
+    const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
+    const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
+    const int per = (js.cpj + kRedSlices - 1) / kRedSlices;
+    const int cb = sl * per, ce = min(js.cpj, cb + per);
+    for (int c = cb; c < ce; c += 8) {
+      float x0[8], x1[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const bool ok = c + u < js.cpj;
-          x0[u] = ok ? __ldg(P + (c + u) * cs + (int64_t)c0 * 128) : 0.f;
-          x1[u] = (ok && c1 >= 0) ? __ldg(P + (c + u) * cs + (int64_t)c1 * 128) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (c + u < js.cpj) {
-            acc += x0[u];
-            if (c1 >= 0) acc += x1[u];
-          }
-        }
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = c + u < ce;
+        x0[u] = ok ? __ldg(P + (c + u) * cs + (int64_t)c0 * 128) : 0.f;
+        x1[u] = (ok && c1 >= 0) ? __ldg(P + (c + u) * cs + (int64_t)c1 * 128) : 0.f;
       }
-      if (r.kind == 2) {
-        if (k == r.in) *r.b_out = acc;
-        else r.w_out[k] = acc;
-      } else {
-        const int mo = m + r.m_off;
-        if (k == r.in) r.b_out[mo] = acc;
-        else r.w_out[(int64_t)mo * r.in + k] = acc;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (c + u < ce) {
+          acc += x0[u];
+          if (c1 >= 0) acc += x1[u];
+        }
       }
     }
-    base += total;
   }
+  part[sl][e_in] = acc;
+  __syncthreads();
+  if (sl == 0 && active) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRedSlices; ++q) t += part[q][e_in];
+    const DwJob& r = js.job[jj];
+    if (r.kind == 2) {
+      if (k == r.in) *r.b_out = t;
+      else r.w_out[k] = t;
+    } else {
+      const int mo = m + r.m_off;
+      if (k == r.in) r.b_out[mo] = t;
+      else r.w_out[(int64_t)mo * r.in + k] = t;
+    }
+  }
+}
+
+static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
+  int64_t total = 0;
+  for (int jj = 0; jj < js.njobs; ++jj) {
+    const DwJob& r = js.job[jj];
+    total += (int64_t)(r.kind == 2 ? 1 : r.rows) * (r.in + 1);
+  }
+  k_dw_reduce<<<(unsigned)((total + 31) / 32), 32 * kRedSlices, 0, st>>>(js);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -590,8 +617,7 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
     cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, st);
     if (e != cudaSuccess) return e;
-    k_dw_reduce<<<64, 256, 0, st>>>(fj);
-    return cudaGetLastError();
+    return launch_dw_reduce(fj, st);
   }
   // dW jobs (image pointers are the same for every micro-batch)
   DwJobs js{};
@@ -628,8 +654,7 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   }
   if (e != cudaSuccess) return e;
   // 4. fixed-order reduction of all partials into the gradient blob
-  k_dw_reduce<<<64, 256, 0, st>>>(js);
-  return cudaGetLastError();
+  return launch_dw_reduce(js, st);
 }
 
 }  // namespace nb
