@@ -1,3 +1,3 @@
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_gpu.log
-for c in c2 c3 c4 c5; do timeout 300 python tools/trainbench.py $c 30; done > gpurun_out/train.log 2>&1
-cat gpurun_out/pytest_gpu.log gpurun_out/train.log
+for i in 1 2 3; do timeout 300 python tools/quickbench.py c2 22; NB_LIB=split timeout 300 python tools/quickbench.py c2 22; done > gpurun_out/quick.log 2>&1
+NB_LIB=split timeout 600 python -m pytest tests -m gpu -x -q -k "c2" 2>&1 | tail -2 >> gpurun_out/quick.log
+cat gpurun_out/quick.log
