@@ -199,22 +199,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
-// Shared-memory flag / counter operations with acquire-release semantics at
-// CTA scope (the chunk hand-off of the fused forward kernel).
-__device__ __forceinline__ uint32_t atom_add_acqrel_smem(uint32_t addr, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ uint32_t ld_acquire_smem(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_smem(uint32_t addr, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
 // One lane of the (converged) warp returns true (elect.sync).
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

@@ -373,11 +373,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
     const uint32_t qb = (uint32_t)(kTile * d0 * 4);
     const uint32_t bar = stage_bar(s, b);
-#ifdef NB_EXP_NOY  // measurement variant: labels not loaded
-    constexpr bool kY = false;
-#else
     constexpr bool kY = MODE != kForward;
-#endif
     mbar_arrive_expect_tx(bar, qb + (kY ? (uint32_t)kTile : 0u));
     bulk_g2s(smem_u32(q_stage(s, b)), p.a.q + t * kTile * d0, qb, bar);
     if (kY) bulk_g2s(smem_u32(y_stage(s, b)), p.a.y + t * kTile, kTile, bar);
@@ -395,9 +391,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         const float* qs = q_stage(s, b) + rit * d0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) x[j] = j < d0 ? qs[j] : 0.f;
-#ifndef NB_EXP_NOY
         ycur = MODE != kForward ? (int)y_stage(s, b)[rit] : 0;
-#endif
       } else {
         const int64_t r = t * kTile + rit;
         const bool v = r < n;
@@ -579,9 +573,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
         }
       } else {
-#ifndef NB_EXP_NOCLS  // measurement variant: no classification
         classify_row_smem<MODE, NHC>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
-#endif
       }
     }
     tile = next;
@@ -598,9 +590,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     tmem_dealloc<COLS>(tmem);
   }
   if (MODE == kScore && warp == 1) flush_cta_counts(ctr, NEPI, NHC == 0 ? -1 : NH, p.a.counts);
-#ifndef NB_EXP_NOFIN  // measurement variant: no count finalisation
   if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a, NHC == 0);
-#endif
 }
 
 // Trace buffer of NB_TRACE builds (defined in nb_fwd_tc.cu).
