@@ -33,8 +33,10 @@
  *    returned are GLOBAL (one NCCL allreduce each); nb_train_step allreduces
  *    the gradient.  All ranks must issue collective calls in the same order.
  *  - Threading: one writer per model (train_step, calibrate, set_*);
- *    concurrent nb_forward / nb_score on distinct streams are allowed when the
- *    model has no communicator.
+ *    concurrent nb_forward / nb_encode calls on distinct streams are allowed.
+ *    nb_score / nb_score_async / nb_score_host / nb_calibrate use the model's
+ *    counter scratch (two alternating sets) and must be issued in order on one
+ *    stream per model (they may interleave with nb_forward on it).
  */
 #ifndef NB_H
 #define NB_H

@@ -458,7 +458,9 @@ static FwdArgs base_args(const nb_model* m, const float* q, const uint8_t* y, in
   for (int k = 0; k < 3; ++k) a.tau[k] = m->tau[k];
   a.counts = m->d_counts;
   a.fin_out = m->d_counts + kFinOff;  // finalised totals (score mode)
-  a.ticket = m->d_flags + 2;     // last-CTA ticket, zero between launches
+  a.ticket = m->d_flags + 2;          // last-CTA ticket
+  a.counts_next = m->d_counts + 8;
+  a.ticket_next = m->d_flags + 3;
   a.fin_add = 0;
   a.keys = m->d_keys;
   a.flags = m->d_flags;
@@ -510,6 +512,17 @@ nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n,
   return NB_OK;
 }
 
+// Score launches alternate between two counter sets / tickets: each launch's
+// finalising CTA zeroes the other set, which the next launch uses.
+static void use_score_set(nb_model* m, FwdArgs& a) {
+  const int p = m->score_parity;
+  m->score_parity ^= 1;
+  a.counts = m->d_counts + 8 * p;
+  a.counts_next = m->d_counts + 8 * (1 - p);
+  a.ticket = m->d_flags + 2 + p;
+  a.ticket_next = m->d_flags + 3 - p;
+}
+
 static void counts_out(const unsigned long long* c, nb_counts* out) {
   out->tp = c[0]; out->fp = c[1]; out->fn = c[2]; out->tn = c[3];
   for (int k = 0; k < 4; ++k) out->exit_hist[k] = c[4 + k];
@@ -523,8 +536,13 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* fin = m->d_counts + kFinOff;
-  if (n > 0) NB_CUDA(launch_forward_any(m, kScore, base_args(m, q, y, n), s));
-  else NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
+  if (n > 0) {
+    FwdArgs a = base_args(m, q, y, n);
+    use_score_set(m, a);
+    NB_CUDA(launch_forward_any(m, kScore, a, s));
+  } else {
+    NB_CUDA(cudaMemsetAsync(fin, 0, sizeof(unsigned long long) * kNumCounters, s));
+  }
   if (m->comm && comm_allreduce_u64_sum(m, fin, kNumCounters, s)) return NB_E_NCCL;
   unsigned long long* hc = m->h_pinned;
   NB_CUDA(cudaMemcpyAsync(hc, fin, sizeof(unsigned long long) * kNumCounters,
@@ -562,6 +580,7 @@ nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, i
     return NB_OK;
   }
   FwdArgs a = base_args(m, q, y, n);
+  use_score_set(m, a);
   if (!m->comm) {  // one launch: the last CTA writes the totals straight into `out`
     a.fin_out = (unsigned long long*)dout;
     NB_CUDA(launch_forward_any(m, kScore, a, s));
@@ -607,6 +626,7 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
     NB_CUDA(cudaEventRecord(m->ev_copy[b], m->copy_stream));
     NB_CUDA(cudaStreamWaitEvent(s, m->ev_copy[b], 0));
     FwdArgs a = base_args(m, m->stage_q[b], m->stage_y[b], rows);
+    use_score_set(m, a);
     a.fin_add = 1;  // every chunk's last CTA adds its totals into fin
     NB_CUDA(launch_forward_any(m, kScore, a, s));
     NB_CUDA(cudaEventRecord(m->ev_done[b], s));

@@ -120,25 +120,24 @@ __device__ __forceinline__ void finalize_counts(const FwdArgs& a, bool raw = fal
   if (t == gridDim.x * gridDim.y * gridDim.z - 1) {
     __threadfence();
     unsigned long long v = 0;
-    if (lane < kNumCounters) v = atomicExch(a.counts + lane * kCtrStride, 0ull);
+    if (lane < kNumCounters) v = __ldcg(a.counts + lane * kCtrStride);
     if (raw) {
       const unsigned long long tp = __shfl_sync(0xFFFFFFFFu, v, 0), pred = __shfl_sync(0xFFFFFFFFu, v, 1);
       const unsigned long long pos = __shfl_sync(0xFFFFFFFFu, v, 2), n = (unsigned long long)a.n;
-      const unsigned long long t[kNumCounters] = {tp, pred - tp, pos - tp, n - pred - pos + tp,
-                                                  0ull, 0ull, n - pred, pred, 0ull};
+      const unsigned long long tt[kNumCounters] = {tp, pred - tp, pos - tp, n - pred - pos + tp,
+                                                   0ull, 0ull, n - pred, pred, 0ull};
 #pragma unroll
       for (int i = 0; i < kNumCounters - 1; ++i)
-        if (lane == i) v = t[i];
+        if (lane == i) v = tt[i];
     }
     if (lane < kNumCounters) {
       if (a.fin_add) atomicAdd(a.fin_out + lane, v);
       else a.fin_out[lane] = v;
+      // re-arm the idle set for the next launch (this set is re-armed by it);
+      // host-mapped fin_out is visible at kernel completion
+      a.counts_next[lane * kCtrStride] = 0ull;
     }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();  // (host-mapped fin_out is visible at kernel completion)
-      atomicExch(a.ticket, 0u);
-    }
+    if (lane == 0) *a.ticket_next = 0u;
   }
 }
 

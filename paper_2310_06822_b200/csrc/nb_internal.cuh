@@ -16,7 +16,7 @@ constexpr int kMaxLayers = 8;
 constexpr int kTile = 128;          // rows per MMA tile (M = 128)
 constexpr int kEncK = 16;           // layer-1 K after the bf16 (hi, lo) split
 constexpr int kNumCounters = 9;     // tp fp fn tn exit[4] nonfinite
-constexpr int kCtrStride = 16;      // device counters 128 B apart (one L2 line each)
+constexpr int kCtrStride = 16;      // device counters 128 B apart (one L2 line each); set 1 at +8
 constexpr int kFinOff = kNumCounters * kCtrStride;  // nb_model::d_counts: finalised totals
 constexpr int kZeroOff = kFinOff + 16;              // ... and a block that stays zero
 constexpr uint32_t kFlagNonFinite = 1u, kFlagLabel = 2u;
@@ -87,7 +87,8 @@ struct nb_model {
   float* d_tau = nullptr;     // [3]
   unsigned long long* d_counts = nullptr;  // counters (strided), totals, zeros: 256 words
   unsigned int* d_keys = nullptr;          // [3] order-preserving min keys
-  unsigned int* d_flags = nullptr;         // sticky flags
+  unsigned int* d_flags = nullptr;         // sticky flags, [2], [3] score tickets
+  int score_parity = 0;                    // counter set of the next score launch
   double* d_loss = nullptr;                // [1]
   unsigned long long* d_stats = nullptr;   // [4] batch tp fp fn tn
   unsigned long long* h_pinned = nullptr;  // pinned host mirror for small readbacks
@@ -152,6 +153,10 @@ struct FwdArgs {
   unsigned long long* fin_out;
   unsigned int* ticket;
   int fin_add;
+  // the other (idle) counter set and ticket: the finalising CTA zeroes them for
+  // the next launch, which uses them (launches alternate between two sets)
+  unsigned long long* counts_next;
+  unsigned int* ticket_next;
   unsigned int* keys;
   unsigned int* flags;
   TrainArgs tr;
