@@ -169,7 +169,10 @@ nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                        void* stream);
 
 /* a1-a5: fused forward + classify + count with the model's thresholds:
- * yhat = [e_1 >= tau_1] and [e_2 >= tau_2] and [z >= tau]; counts to *out (host). */
+ * yhat = [e_1 >= tau_1] and [e_2 >= tau_2] and [z >= tau]; counts to *out (host).
+ * Records with a non-finite logit are counted in out->nonfinite (a NaN never
+ * passes z >= tau) and make the call return the warning-class NB_E_NONFINITE
+ * with the counts written.                                                  */
 nb_status nb_score(const nb_model* m, const float* q, const uint8_t* y, int64_t n,
                    nb_counts* out, void* stream);
 /* Asynchronous nb_score: the same kernel, allreduce and counts, but the counts

@@ -29,7 +29,7 @@ FP32, BF16 = 0, 1
 PRECISIONS = {"fp32": FP32, "bf16": BF16}
 STATUS = ["NB_OK", "NB_E_ARG", "NB_E_SHAPE", "NB_E_NONFINITE", "NB_E_LABEL",
           "NB_E_NO_POSITIVES", "NB_E_CUDA", "NB_E_NCCL", "NB_E_UNSUPPORTED", "NB_E_OOM"]
-NB_OK, NB_E_NO_POSITIVES = 0, 5
+NB_OK, NB_E_NONFINITE, NB_E_NO_POSITIVES = 0, 3, 5
 
 
 class NBError(RuntimeError):
@@ -289,10 +289,11 @@ class Model:
                                   n, tau.data_ptr(), _stream(self.device)), "nb_calibrate", ok)
         return tau
 
-    def score(self, q: torch.Tensor, y: torch.Tensor) -> dict:
+    def score(self, q: torch.Tensor, y: torch.Tensor, allow_nonfinite: bool = False) -> dict:
         c = _Counts()
+        ok = (NB_OK, NB_E_NONFINITE) if allow_nonfinite else (NB_OK,)
         _check(lib().nb_score(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
-                              q.shape[0], C.byref(c), _stream(self.device)), "nb_score")
+                              q.shape[0], C.byref(c), _stream(self.device)), "nb_score", ok)
         return c.as_dict()
 
     def score_async(self, q: torch.Tensor, y: torch.Tensor, out: torch.Tensor) -> None:

@@ -549,7 +549,12 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
                           cudaMemcpyDeviceToHost, s));
   NB_CUDA(cudaStreamSynchronize(s));
   counts_out(hc, out);
-  return take_flags(m, s, NB_OK);
+  nb_status st = take_flags(m, s, NB_OK);
+  if (st == NB_OK && out->nonfinite) {  // warning-class: the counts are written
+    set_error("%llu records produced a non-finite logit", (unsigned long long)out->nonfinite);
+    st = NB_E_NONFINITE;
+  }
+  return st;
 }
 
 // Device-visible address of `out` (device memory, or pinned host memory mapped
@@ -637,7 +642,12 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
                           cudaMemcpyDeviceToHost, s));
   NB_CUDA(cudaStreamSynchronize(s));
   counts_out(hc, out);
-  return take_flags(m, s, NB_OK);
+  nb_status st = take_flags(m, s, NB_OK);
+  if (st == NB_OK && out->nonfinite) {  // warning-class: the counts are written
+    set_error("%llu records produced a non-finite logit", (unsigned long long)out->nonfinite);
+    st = NB_E_NONFINITE;
+  }
+  return st;
 }
 
 nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,

@@ -335,6 +335,14 @@ __device__ __forceinline__ void mma_commit2(uint32_t bar) {
 }
 
 
+// ReLU that keeps NaN (max.NaN): a non-finite record's NaN survives the last
+// hidden layer into the logit (R26) at the cost of a plain FMNMX.
+__device__ __forceinline__ float relu_nan(float x) {
+  float r;
+  asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // relu + round-to-nearest-even pack of two fp32 into bf16x2 (lo = a, hi = b)
 __device__ __forceinline__ uint32_t pack_relu_bf16x2(float a, float b) {
   uint32_t r;

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         }
         if (l == h0 || l == h1 || last) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
+          for (int i = 0; i < 32; ++i) t[i] = relu_nan(t[i]);
           const int o = 32 * c;
           // head vectors: 16-B aligned (pack layout, col0 % 32 == 0) -> LDS.128
           auto dot = [&](float& sa, float& sb, const float* w) {
@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     if (lead) {
       const int64_t r = tile * kTile + rit;
       const bool valid = r < n;
+      if (MODE == kCalibrate && valid && !isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
       if (MODE == kForward) {
         if (valid) {
           p.a.logits[r * nl] = z;

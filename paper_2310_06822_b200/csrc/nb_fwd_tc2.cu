@@ -333,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
         }
         if (l == h0 || l == h1 || last) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = fmaxf(t[i], 0.f);
+          for (int i = 0; i < 32; ++i) t[i] = relu_nan(t[i]);
           const int o = 32 * c;
           if (l == h0) {
 #pragma unroll
@@ -375,6 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
       }
       const int64_t r = half_base(tile) + rit;
       const bool valid = r < n;
+      if (MODE == kCalibrate && valid && !isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
       if (MODE == kForward) {
         if (valid) {
           p.a.logits[r * nl] = z;

@@ -217,10 +217,13 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
     const bool valid = i < a.n;
     float h[W];
     float e[2] = {0.f, 0.f};
+    bool bad = false;
     {
       float x[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] = (valid && j < s.d0) ? a.q[i * s.d0 + j] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bad = bad || (j < s.d0 && !isfinite(x[j]));
       const float* W0 = sp + s.po.W[0];
       const float* b0 = sp + s.po.b[0];
 #pragma unroll
@@ -260,6 +263,8 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
 #pragma unroll
       for (int j = 0; j < W; ++j) z = fmaf(wo[j], h[j], z);
     }
+    if (bad) z = __int_as_float(0x7FC00000);  // non-finite record -> NaN logit (R26)
+    if (MODE == kCalibrate && valid && !isfinite(z)) atomicOr(a.flags, kFlagNonFinite);
     if (MODE == kForward) {
       if (valid) {
         a.logits[i * nl] = z;

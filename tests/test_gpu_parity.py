@@ -435,3 +435,41 @@ def test_train_micro_batches_equal_one_batch(name, monkeypatch):
     assert all(s1[k] == s2[k] for k in ("tp", "fp", "fn", "tn"))
     assert abs(s1["loss"] - s2["loss"]) <= 1e-5 * abs(s1["loss"])
     assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+def test_nonfinite_records(name):
+    """Non-finite input ("non-finite input -> error"; R26):
+    nb_score counts the rows whose logit is not finite, never predicts them
+    positive when NaN, and returns the warning-class NB_E_NONFINITE with the
+    counts written; nb_forward's NaN logits surface as NB_E_NONFINITE on the
+    next synchronising call."""
+    cfg = nbgen.CONFIGS[name]
+    n = 128 * 3 + 9
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 9))
+    qd, yd = cuda(q), cuda(y)
+    m.calibrate(qd, yd, allow_no_positives=True)
+    ref = m.score(qd, yd)
+    bad = q.clone()
+    rows = [0, 130, n - 1]
+    for r in rows:
+        bad[r, 0] = float("nan")
+    with pytest.raises(nb.NBError) as ei:
+        m.score(cuda(bad), yd)
+    assert "NONFINITE" in str(ei.value)
+    c = m.score(cuda(bad), yd, allow_nonfinite=True)
+    assert c["nonfinite"] == len(rows)
+    assert c["tp"] + c["fp"] + c["fn"] + c["tn"] == n
+    # a non-finite record's logit is NaN, which never passes z >= tau: those rows
+    # move to the predicted-negative side, every other row is unchanged
+    z0 = m.forward(qd)
+    predpos = (z0[rows, 0].cpu() >= m.get_thresholds()[0]).numpy()
+    pos_bad = [r for r, pp in zip(rows, predpos) if pp]
+    assert c["tp"] + c["fp"] == ref["tp"] + ref["fp"] - len(pos_bad)
+    z = m.forward(cuda(bad))
+    assert torch.isnan(z[rows, 0]).all() and torch.isfinite(z[[1, 2, 129], 0]).all()
+    with pytest.raises(nb.NBError):
+        m.calibrate(qd, yd, allow_no_positives=True)  # reports the forward's flag
