@@ -473,3 +473,50 @@ def test_nonfinite_records(name):
     assert torch.isnan(z[rows, 0]).all() and torch.isfinite(z[[1, 2, 129], 0]).all()
     with pytest.raises(nb.NBError):
         m.calibrate(qd, yd, allow_no_positives=True)  # reports the forward's flag
+
+
+def test_nccl_communicator_world1():
+    """The NCCL path of nb_comm_init / the in-library allreduces on a real GPU
+    (world size 1 on the one-GPU box; the multi-rank host logic is covered by
+    the gloo tests): calibrate, score, score_async and a training step with a
+    communicator give the results of the same model without one."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2310_06822_b200.dist import comm_init
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", DEV))
+    try:
+        cfg = nbgen.CONFIGS["c2"]
+        n = 128 * 50 + 3
+        q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+        y = labels_oracle(cfg, q.numpy())
+        qd, yd = cuda(q), cuda(y)
+        th = scaled_params(cfg, 9)
+        out = []
+        for with_comm in (False, True):
+            m = nb.Model(desc_of(cfg), DEV)
+            if with_comm:
+                comm_init(m)
+            m.set_params(th)
+            tau = m.calibrate(qd, yd)
+            c = m.score(qd, yd)
+            h = torch.zeros(9, dtype=torch.int64).pin_memory()
+            m.score_async(qd, yd, h)
+            torch.cuda.synchronize()
+            st = m.train_step(qd, yd, alpha=5.0, stats=True)
+            out.append((tau, c, m.counts_dict(h), st, m.get_grad()))
+        (t0, c0, a0, s0, g0), (t1, c1, a1, s1, g1) = out
+        assert torch.equal(t0, t1) and c0 == c1 and a0 == a1 == c0
+        assert all(s0[k] == s1[k] for k in ("tp", "fp", "fn", "tn"))
+        assert torch.equal(g0, g1)
+    finally:
+        dist.destroy_process_group()
