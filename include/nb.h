@@ -201,6 +201,37 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
  * beta_t = 1.                                                               */
 double nb_alpha(int64_t t, int64_t T);
 
+/* ---- the paper's training control (Suppl.
+ * §2.1-2.2; readings DESIGN.md R37-R39) --------------------------- */
+/* L1 / L2 regularisation: every later nb_train_step's Adam adds
+ * l1 sign(theta) + 2 l2 theta to the gradient (all parameters). >= 0.        */
+nb_status nb_model_set_regularization(nb_model* m, float l1, float l2);
+
+/* FN-gated step schedule.  Every step_every training steps ("every 10,000
+ * iterations") the window's summed batch FN (nb_step_stats.fn) is
+ * inspected: if it is not 0, the k-th such trigger lowers the FP weight beta
+ * by base / k (base 1/20, 1/100, 1/200 for 2D, 3D, 4D, Suppl. §2.1's harmonic
+ * decrements, floored at 1e-3) and raises the FN weight alpha by 0.2 (R37);
+ * lambda (used for both l1 and l2) grows linearly from 0 to 5e-7 over
+ * max_steps (Suppl. §2.2, R38); stop is set once 6 consecutive windows had
+ * FN = 0 (R39) or max_steps steps were taken.  Host-only, no GPU.   */
+typedef struct {
+  int32_t space_dim;
+  int32_t patience;        /* stable windows before stopping (6)             */
+  int64_t step_every;      /* window length in steps (10,000 in the paper)   */
+  int64_t max_steps;       /* iteration cap (lambda ramp length)             */
+  double alpha, beta;      /* weights for the next nb_train_step             */
+  double lambda;           /* regularisation weight for the next step        */
+  int64_t step;            /* steps reported so far                          */
+  int64_t triggers;        /* windows with FN > 0 so far                     */
+  uint64_t window_fn;      /* FN summed over the current window              */
+  int32_t stable;          /* consecutive windows with FN = 0                */
+  int32_t stop;            /* early-stop / cap reached                       */
+} nb_schedule;
+nb_status nb_schedule_init(nb_schedule* s, int32_t space_dim, int64_t step_every, int64_t max_steps);
+/* Report one finished step's batch FN; updates alpha, beta, lambda, stop.   */
+nb_status nb_schedule_after_step(nb_schedule* s, uint64_t batch_fn);
+
 /* ---- ground-truth labeller (harness support, not a hot-path row) ----------- */
 /* Occupancy grid uint8 host array, row-major, axis 0 slowest; 4D grids are
  * [frames][R][R][R].  Builds a summed-area table on the device for boxes.   */

@@ -3,7 +3,8 @@
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
 cpu_baseline / --impl reference legs of bench.py, never by the product package
 (paper_2310_06822_b200).  It shares no code with the CUDA path; see
-oracle/nb_oracle.h for the per-function citations into PAPER.md.
+oracle/nb_oracle.h for the per-function citations into PAPER.md.  The training
+control (PaperSchedule, reg_grad; NEXT-2) is plain Python/numpy in this file.
 """
 from __future__ import annotations
 
@@ -182,6 +183,48 @@ def adam(theta, m, v, t, g, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
     """In-place Adam on float64 numpy arrays."""
     lib().ora_adam(theta.size, _ptr(theta), _ptr(m), _ptr(v), t, lr, b1, b2, eps,
                    _ptr(_np(g, np.float64)))
+
+
+def reg_grad(theta, l1, l2) -> np.ndarray:
+    """Gradient of l1 sum|theta| + l2 sum theta^2 (Suppl. Sec. 2.2 "L1 and L2
+    regularizations", P:762-764; DESIGN.md R38: every parameter)."""
+    th = _np(theta, np.float64)
+    return l1 * np.sign(th) + 2.0 * l2 * th
+
+
+class PaperSchedule:
+    """Suppl. Sec. 2.1 FN-gated weight schedule and the early stop
+    of P:297, step by step in the paper's terms (R37-R39): every
+    `step_every` iterations, if the window saw FNs, the k-th such step moves
+    the weights by the dimension's harmonic decrement (1/20, 1/40, ... in 2D;
+    1/100, 1/200, ... in 3D; 1/200, 1/400, ... in 4D) on the FP side (beta,
+    floor 1e-3) and by 0.2 on the FN side (alpha); lambda ramps linearly from
+    0 to 5e-7 (Suppl. Sec. 2.2); training stops after six FN-free windows."""
+
+    def __init__(self, space_dim, step_every=10000, max_steps=1 << 40):
+        self.space_dim, self.step_every, self.max_steps = space_dim, step_every, max_steps
+        self.alpha, self.beta, self.lam = 1.0, 1.0, 0.0
+        self.step = self.triggers = self.window_fn = self.stable = 0
+        self.stop = False
+
+    def decrement(self, k):
+        first = {2: 20.0, 3: 100.0, 4: 200.0}[self.space_dim]
+        return 1.0 / (first * k)  # 1/20, 1/40, 1/60 ... (2D)
+
+    def after_step(self, batch_fn):
+        self.window_fn += int(batch_fn)
+        self.step += 1
+        if self.step % self.step_every == 0:
+            if self.window_fn > 0:
+                self.triggers += 1
+                self.beta = max(1e-3, self.beta - self.decrement(self.triggers))
+                self.alpha = self.alpha + 0.2
+                self.stable = 0
+            else:
+                self.stable += 1
+            self.window_fn = 0
+        self.lam = 5e-7 * min(1.0, self.step / self.max_steps)
+        self.stop = self.stable >= 6 or self.step >= self.max_steps
 
 
 def alpha(t, T) -> float:

@@ -54,6 +54,33 @@ class _Counts(C.Structure):
                     exit_hist=list(self.exit_hist), nonfinite=self.nonfinite)
 
 
+class _Schedule(C.Structure):
+    _fields_ = [("space_dim", C.c_int32), ("patience", C.c_int32), ("step_every", C.c_int64),
+                ("max_steps", C.c_int64), ("alpha", C.c_double), ("beta", C.c_double),
+                ("lam", C.c_double), ("step", C.c_int64), ("triggers", C.c_int64),
+                ("window_fn", C.c_uint64), ("stable", C.c_int32), ("stop", C.c_int32)]
+
+
+class PaperSchedule:
+    """The paper's FN-gated training control (nb_schedule_*, nb.h): alpha, beta
+    and the L1/L2 weight for the next step; report each step's batch FN."""
+
+    def __init__(self, space_dim: int, step_every: int = 10000, max_steps: int = 1 << 40):
+        self._s = _Schedule()
+        _check(lib().nb_schedule_init(C.byref(self._s), space_dim, step_every, max_steps),
+               "nb_schedule_init")
+
+    def after_step(self, batch_fn: int) -> None:
+        _check(lib().nb_schedule_after_step(C.byref(self._s), int(batch_fn)), "nb_schedule_after_step")
+
+    alpha = property(lambda self: self._s.alpha)
+    beta = property(lambda self: self._s.beta)
+    lam = property(lambda self: self._s.lam)
+    triggers = property(lambda self: self._s.triggers)
+    step = property(lambda self: self._s.step)
+    stop = property(lambda self: bool(self._s.stop))
+
+
 class _Stats(C.Structure):
     _fields_ = [("loss", C.c_double), ("tp", C.c_uint64), ("fp", C.c_uint64),
                 ("fn", C.c_uint64), ("tn", C.c_uint64)]
@@ -89,6 +116,9 @@ SIGNATURES = {
     "nb_score_async": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
     "nb_alpha": (_D, [_I64, _I64]),
+    "nb_model_set_regularization": (C.c_int, [_P, _F, _F]),
+    "nb_schedule_init": (C.c_int, [_P, _I32, _I64, _I64]),
+    "nb_schedule_after_step": (C.c_int, [_P, C.c_uint64]),
     "nb_grid_create": (C.c_int, [_I32, _I32, _I32, _P, _I32, _P]),
     "nb_grid_destroy": (None, [_P]),
     "nb_label": (C.c_int, [_P, _I32, _P, _I64, _P, _P]),
@@ -323,6 +353,9 @@ class Model:
         _check(lib().nb_score_host(self._h, q.data_ptr(), y.data_ptr(), q.shape[0], C.byref(c),
                                    _stream(self.device)), "nb_score_host")
         return c.as_dict()
+
+    def set_regularization(self, l1: float, l2: float) -> None:
+        _check(lib().nb_model_set_regularization(self._h, l1, l2), "nb_model_set_regularization")
 
     def train_step(self, q, y, alpha: float, beta: float = 1.0, lr: float = 1e-3,
                    n_global: int | None = None, stats: bool = False):

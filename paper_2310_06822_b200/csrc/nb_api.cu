@@ -706,6 +706,48 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   return NB_OK;
 }
 
+nb_status nb_model_set_regularization(nb_model* m, float l1, float l2) {
+  if (!m || !(l1 >= 0.f) || !(l2 >= 0.f)) return set_error("bad argument"), NB_E_ARG;
+  m->l1 = l1;
+  m->l2 = l2;
+  return NB_OK;
+}
+
+nb_status nb_schedule_init(nb_schedule* s, int32_t space_dim, int64_t step_every, int64_t max_steps) {
+  if (!s || space_dim < 2 || space_dim > 4 || step_every < 1 || max_steps < 1)
+    return set_error("bad argument"), NB_E_ARG;
+  memset(s, 0, sizeof(*s));
+  s->space_dim = space_dim;
+  s->patience = 6;
+  s->step_every = step_every;
+  s->max_steps = max_steps;
+  s->alpha = 1.0;
+  s->beta = 1.0;
+  s->lambda = 0.0;
+  return NB_OK;
+}
+
+nb_status nb_schedule_after_step(nb_schedule* s, uint64_t batch_fn) {
+  if (!s) return set_error("null argument"), NB_E_ARG;
+  s->window_fn += batch_fn;
+  s->step += 1;
+  if (s->step % s->step_every == 0) {  // end of a scheduling window
+    if (s->window_fn > 0) {
+      s->triggers += 1;
+      const double base = s->space_dim == 2 ? 1.0 / 20 : (s->space_dim == 3 ? 1.0 / 100 : 1.0 / 200);
+      s->beta = std::max(1e-3, s->beta - base / (double)s->triggers);
+      s->alpha = 1.0 + 0.2 * (double)s->triggers;
+      s->stable = 0;
+    } else {
+      s->stable += 1;
+    }
+    s->window_fn = 0;
+  }
+  s->lambda = 5e-7 * std::min(1.0, (double)s->step / (double)s->max_steps);
+  if (s->stable >= s->patience || s->step >= s->max_steps) s->stop = 1;
+  return NB_OK;
+}
+
 double nb_alpha(int64_t t, int64_t T) {
   if (T <= 1) return 1000.0;
   return 1.0 + 999.0 * (double)t / (double)(T - 1);

@@ -80,6 +80,7 @@ struct nb_model {
   float* adam_v = nullptr;
   float* grad = nullptr;      // [P] gradient of the current step
   int64_t step = 0;
+  float l1 = 0.f, l2 = 0.f;   // L1 / L2 regularisation added to the gradient by Adam (R38)
   uint8_t* packed = nullptr;  // bf16 packed image (pl.bytes)
   nb::BwdLayout bl;
   uint8_t* packed_bwd = nullptr;  // w = 256 training: 2 transposed pair images (bl.bytes)

@@ -596,12 +596,18 @@ cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int
 // ---------------------------------------------------------------------------
 // Adam (PyTorch semantics, R8) on the fp32 master weights.
 // ---------------------------------------------------------------------------
+// L1 + L2 regularisation (Suppl. §2.2; R38): the
+// gradient of l1 * sum |theta| + l2 * sum theta^2 over all parameters.
+__device__ __forceinline__ float reg_grad(float t, float l1, float l2) {
+  return l1 * (t > 0.f ? 1.f : (t < 0.f ? -1.f : 0.f)) + 2.f * l2 * t;
+}
+
 __global__ void k_adam(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, int64_t P, float lr_over_bc1,
-                       float inv_sqrt_bc2, float b1, float b2, float eps) {
+                       float inv_sqrt_bc2, float b1, float b2, float eps, float l1, float l2) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float gi = g[i];
+    float gi = g[i] + reg_grad(th[i], l1, l2);
     float mi = b1 * m[i] + (1.f - b1) * gi;
     float vi = b2 * v[i] + (1.f - b2) * gi * gi;
     m[i] = mi;
@@ -621,11 +627,12 @@ __device__ __forceinline__ void store_bf16(uint8_t* img, int K, int n, int k, fl
 
 __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                             const float* __restrict__ g, int64_t P, float lr_over_bc1,
-                            float inv_sqrt_bc2, float b1, float b2, float eps, PackArgs a) {
+                            float inv_sqrt_bc2, float b1, float b2, float eps, float l1, float l2,
+                            PackArgs a) {
   const int W = a.W, rows = W / (int)a.pl.pairs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
+    const float gi = g[i] + reg_grad(th[i], l1, l2);
     const float mi = b1 * m[i] + (1.f - b1) * gi;
     const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
     m[i] = mi;
@@ -705,7 +712,7 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
   k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P,
                                      (float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1,
-                                     (float)b2, (float)eps, a);
+                                     (float)b2, (float)eps, m->l1, m->l2, a);
   return cudaGetLastError();
 }
 
@@ -716,7 +723,7 @@ cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s) {
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
   k_adam<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P,
                                 (float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1, (float)b2,
-                                (float)eps);
+                                (float)eps, m->l1, m->l2);
   return cudaGetLastError();
 }
 

@@ -520,3 +520,66 @@ def test_nccl_communicator_world1():
         assert torch.equal(g0, g1)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+def test_regularized_adam_step(name):
+    """NEXT-2 (Suppl. §2.2, R38): with L1/L2 set, the step's Adam update uses
+    g + l1 sign(theta) + 2 l2 theta over every parameter (fp32 SIMT, fused w=64
+    and CTA-pair paths); get_grad stays the pure Eq. (1) gradient."""
+    cfg = nbgen.CONFIGS[name]
+    B = 3 * 1024 + 5
+    q = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, B)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 4).double().numpy()
+    th[::7] = 0.0                                   # sign(0) = 0 on both sides
+    l1, l2 = 3e-3, 0.4
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(torch.from_numpy(th).float())
+    m.set_regularization(l1, l2)
+    m.train_step(cuda(q), cuda(y), alpha=5.0, beta=0.8, lr=1e-3)
+    g = m.get_grad().double().numpy()
+    th32 = torch.from_numpy(th).float().double().numpy()
+    ref = th32.copy()
+    mm, vv = np.zeros_like(ref), np.zeros_like(ref)
+    oracle.adam(ref, mm, vv, 1, g + oracle.reg_grad(th32, l1, l2))
+    noreg = th32.copy()
+    oracle.adam(noreg, np.zeros_like(ref), np.zeros_like(ref), 1, g)
+    th1 = m.get_params().double().numpy()
+    assert np.allclose(th1, ref, atol=2e-6)
+    assert not np.allclose(th1, noreg, atol=2e-6)   # the terms did act
+    # the gradient itself is not regularised
+    _, gr, _ = oracle.loss_grad(oracle.arch_of(cfg), th32, q.numpy(), y, 5.0, 0.8,
+                                mode=oracle.FP64 if cfg.precision == "fp32" else oracle.BF16_EMU)
+    assert np.linalg.norm(g - gr) <= 2e-2 * np.linalg.norm(gr)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_paper_training_control_run(name):
+    """NEXT-2 end to end: training driven by the paper's control (R37-R39):
+    the batch FN the kernels report feed nb_schedule_after_step, its alpha,
+    beta and lambda drive the next step.  The schedule equals the oracle's on
+    the same FN sequence, and the calibrated network keeps FN = 0."""
+    cfg = nbgen.CONFIGS[name]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 1 << 16)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(nbgen.init_params(cfg))
+    s = nb.PaperSchedule(cfg.space_dim, step_every=5, max_steps=120)
+    o = oracle.PaperSchedule(cfg.space_dim, step_every=5, max_steps=120)
+    fns = []
+    while not s.stop:
+        t = s.step
+        m.set_regularization(s.lam, s.lam)
+        sl = slice((t % 16) * 4096, (t % 16 + 1) * 4096)
+        st = m.train_step(qd[sl], yd[sl], alpha=s.alpha, beta=s.beta, lr=1e-3, stats=True)
+        fns.append(st["fn"])
+        s.after_step(st["fn"])
+        o.after_step(st["fn"])
+        assert (s.alpha, s.beta, s.triggers, s.stop) == \
+            (pytest.approx(o.alpha), pytest.approx(o.beta), o.triggers, o.stop)
+        assert s.lam == pytest.approx(o.lam, abs=1e-20)
+    assert len(fns) <= 120 and sum(fns) > 0 and s.triggers > 0
+    m.calibrate(qd, yd)
+    assert m.score(qd, yd)["fn"] == 0
