@@ -34,6 +34,7 @@ SOURCES = {
     "nb_train_tc.cu": [],
     "nb_train_tc2.cu": [],
     "nb_train_fused.cu": [],
+    "nb_fwd_exit.cu": [],
     "nb_label.cu": ["-fmad=false"],   # exact fp64 DDA rounding (no FMA contraction)
     "nb_comm.cpp": [],
 }

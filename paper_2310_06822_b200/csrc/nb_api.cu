@@ -165,9 +165,19 @@ static void timing_end(const nb_model* m, cudaStream_t s) {
   mm->kernel_launches += 1;
 }
 
+// Measurement / test switch: score models with exit heads densely (every head
+// on every row, nb_fwd_tc.cuh) instead of with early-exit compaction.
+static bool g_dense_exits = false;
+extern "C" void nb_debug_set_dense_exits(int v) { g_dense_exits = v != 0; }
+
 static cudaError_t launch_forward_any(const nb_model* m, int mode, const FwdArgs& a,
                                       cudaStream_t s) {
   timing_begin(m, s);
+  if (mode == kScore && !g_dense_exits && exit_compaction_supported(m)) {
+    cudaError_t e = launch_score_exit(const_cast<nb_model*>(m), a, s);
+    timing_end(m, s);
+    return e;
+  }
   cudaError_t e = m->d.precision != NB_BF16 ? launch_fwd_simt(m, mode, a, s)
                   : m->pl.pairs == 2        ? launch_fwd_tc2(m, mode, a, s)
                                             : launch_fwd_tc(m, mode, a, s);
@@ -327,6 +337,7 @@ void nb_model_destroy(nb_model* m) {
   cudaFree(m->d_flags);
   cudaFree(m->d_loss);
   cudaFree(m->train_scratch);
+  cudaFree(m->exit_scratch);
   for (int i = 0; i < 2; ++i) {
     cudaFree(m->stage_q[i]);
     cudaFree(m->stage_y[i]);
@@ -672,6 +683,7 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   if (need > m->train_scratch_bytes) {
     NB_CUDA(cudaStreamSynchronize(s));
     cudaFree(m->train_scratch);
+  cudaFree(m->exit_scratch);
     m->train_scratch = nullptr;
     m->train_scratch_bytes = 0;
     cudaError_t e = cudaMalloc(&m->train_scratch, need);

@@ -96,6 +96,9 @@ struct nb_model {
   // training scratch (grown on demand outside the timed hot path)
   void* train_scratch = nullptr;
   size_t train_scratch_bytes = 0;
+  // early-exit compaction scratch (nb_fwd_exit.cu): 2 image/label region sets
+  void* exit_scratch = nullptr;
+  size_t exit_scratch_bytes = 0;
   // host-buffer serving path
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
@@ -170,6 +173,8 @@ cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* ou
 cudaError_t launch_fwd_simt(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
+bool exit_compaction_supported(const nb_model* m);
+cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t s);
 bool tc_supported(const nb_desc& d);
 bool tc2_supported(const nb_desc& d);
 bool simt_supported(const nb_desc& d);

@@ -583,3 +583,94 @@ def test_paper_training_control_run(name):
     assert len(fns) <= 120 and sum(fns) > 0 and s.triggers > 0
     m.calibrate(qd, yd)
     assert m.score(qd, yd)["fn"] == 0
+
+
+# ---------------------------------------------------------------- early-exit compaction (K9)
+def _exit_model(n, seed=0):
+    cfg = nbgen.CONFIGS["c4"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, seed, n)
+    y = labels_oracle(cfg, q.numpy())
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 3))
+    return cfg, q, y, m
+
+
+def _score_both(m, qd, yd):
+    L = nb.lib()
+    try:
+        c = m.score(qd, yd, allow_nonfinite=True)
+        L.nb_debug_set_dense_exits(1)
+        d = m.score(qd, yd, allow_nonfinite=True)
+    finally:
+        L.nb_debug_set_dense_exits(0)
+    return c, d
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 2 * 148 * 128 + 77, (1 << 20) + 5])
+def test_exit_compaction_counts_equal_dense(n):
+    """the compacted three-segment score (survivors of each head
+    packed into full tiles) gives exactly the dense kernel's counts and exit
+    histogram; thresholds are set at logit quantiles so both heads exit a
+    sizeable share of rows."""
+    cfg, q, y, m = _exit_model(n)
+    qd, yd = cuda(q), cuda(y)
+    z = m.forward(qd).cpu()
+    m.set_thresholds([float(z[:, 0].median()), float(z[:, 1].quantile(0.4)) if n > 1 else 0.0,
+                      float(z[:, 2].quantile(0.3)) if n > 1 else 0.0])
+    c, d = _score_both(m, qd, yd)
+    assert c == d, (c, d)
+    assert sum(c["exit_hist"]) == n
+    if n > 1000:
+        assert c["exit_hist"][0] > 0.2 * n and c["exit_hist"][1] > 0.05 * n
+
+
+def test_exit_compaction_vs_oracle_and_chunks():
+    """Two compaction chunks (2^22 rows each by default) plus a ragged tail:
+    counts equal the bf16-emulating oracle's outside the 1e-3 band of every
+    threshold (R28), and equal the dense kernel's everywhere."""
+    n = (1 << 22) + 3 * 128 + 11
+    cfg, q, y, m = _exit_model(n, seed=1)
+    qd, yd = cuda(q), cuda(y)
+    z = m.forward(qd).cpu()
+    tau = [float(z[:, 0].median()), float(z[:, 1].quantile(0.5)), float(z[:, 2].quantile(0.2))]
+    m.set_thresholds(tau)
+    c, d = _score_both(m, qd, yd)
+    assert c == d
+    # oracle on a sample of rows away from every threshold
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(n, 40000, replace=False))
+    zs = z[idx].double().numpy()
+    keep = np.all(np.abs(zs - np.array(tau)) >= 1e-3, axis=1)
+    idx = idx[keep]
+    th = m.get_params().double().numpy()
+    zo = oracle.forward(oracle.arch_of(cfg), th, q.numpy()[idx], oracle.BF16_EMU)
+    zo = zo.reshape(len(idx), -1)
+    keep2 = np.all(np.abs(zo - np.array(tau)) >= 1e-3, axis=1)
+    idx, zo = idx[keep2], zo[keep2]
+    sub = m.score(cuda(q.numpy()[idx]), cuda(y[idx]))
+    co = oracle.score(zo, y[idx], np.array(tau, dtype=np.float64))
+    for k in ("tp", "fp", "fn", "tn", "exit_hist"):
+        assert sub[k] == co[k], (k, sub, co)
+    assert co["exit_hist"][0] > 0.3 * len(idx) and co["exit_hist"][1] > 0.05 * len(idx)
+
+
+def test_exit_compaction_nonfinite_and_async_paths():
+    """NaN records exit at head 1 and are counted once as non-finite; the
+    async (device destination) and host-buffer entry points take the same
+    compacted path and agree with nb_score."""
+    n = 3 * 128 * 148 + 19
+    cfg, q, y, m = _exit_model(n, seed=2)
+    z = m.forward(cuda(q)).cpu()
+    m.set_thresholds([float(z[:, 0].median()), float(z[:, 1].quantile(0.4)), float(z[:, 2].quantile(0.4))])
+    bad = q.clone()
+    rows = [0, 200, 9000, n - 1]
+    for r in rows:
+        bad[r, 1] = float("nan")
+    c, d = _score_both(m, cuda(bad), cuda(y))
+    assert c == d and c["nonfinite"] == len(rows)
+    out = torch.zeros(9, dtype=torch.int64, device=f"cuda:{DEV}")
+    m.score_async(cuda(bad), cuda(y), out)
+    assert nb.Model.counts_dict(out.cpu()) == c
+    clean = m.score(cuda(q), cuda(y))
+    h = m.score_host(q.contiguous(), torch.from_numpy(y).contiguous())
+    assert h == clean
