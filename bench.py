@@ -47,7 +47,9 @@ WORKLOAD = {
           "per step sharded over the ranks",
 }
 KERNEL = {"c2": "k_fwd_tc<64,4,0,0,kScore,d0=3,BF>", "c3": "k_fwd_tc<128,4,0,0,kScore,d0=6,BF>",
-          "c4": "k_fwd_tc<128,6,2,4,kScore,d0=4,BF>", "c5": "k_fwd_tc2<4,kScore,BF> (CTA pairs)"}
+          "c4": "k_score_exit<2,{records,image,image},{head1,head2,output}> (early-exit compaction, "
+                "3 segment kernels per 2^24-row chunk)",
+          "c5": "k_fwd_tc2<4,kScore,BF> (CTA pairs)"}
 METRIC = "bounding queries/s"
 UNIT = "queries/s"
 
@@ -58,6 +60,32 @@ def flop_per_query(cfg) -> int:
     macs = cfg.record_floats * cfg.width + (cfg.hidden_layers - 1) * cfg.width ** 2
     macs += cfg.width * (1 + cfg.n_heads)
     return 2 * macs
+
+
+def executed_flop_per_query(cfg, hist, n) -> float:
+    """Algorithmic flops per query actually computed with early exits (c4):
+    layers 1..h1 and head 1 for every row, layers h1+1..h2 and head 2 for the
+    rows that passed head 1, the rest and the output head for rows that passed
+    both."""
+    W = cfg.width
+    h1, h2 = cfg.head_after
+    s1 = (n - hist[0]) / n
+    s2 = (n - hist[0] - hist[1]) / n
+    f0 = cfg.record_floats * W + (h1 - 1) * W * W + W
+    f1 = (h2 - h1) * W * W + W
+    f2 = (cfg.hidden_layers - h2) * W * W + W
+    return 2 * (f0 + s1 * f1 + s2 * f2)
+
+
+def train_for_exits(nb, nbgen, m, grid, cfg, steps, rank, world):
+    """c4's exit heads only skip work once trained: the bench model is trained
+    for `steps` Adam steps with Eq. (1) on fresh TRAIN batches (the config's
+    batch split over the ranks, alpha ramp 1 -> 1000) before calibration."""
+    dev = f"cuda:{m.device}"
+    B = cfg.train_batch
+    for t in range(steps):
+        qt = nbgen.train_batch(cfg, t, rank, world, device=dev)
+        m.train_step(qt, grid.label(cfg.kind, qt), alpha=nb.alpha(t, steps), n_global=B)
 
 
 def load_peaks():
@@ -238,11 +266,16 @@ def run_ours(args):
         from paper_2310_06822_b200.dist import comm_init
 
         comm_init(m)
-    m.set_params(nbgen.init_params(cfg) * 2.5)
     strong = CONFIG in STRONG
     n = N_STEP[CONFIG] // world if strong else N_STEP[CONFIG]
-    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
     grid = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
+    exits = cfg.n_heads > 0 and args.exit_train_steps > 0
+    if exits:
+        m.set_params(nbgen.init_params(cfg))
+        train_for_exits(nb, nbgen, m, grid, cfg, args.exit_train_steps, rank, world)
+    else:
+        m.set_params(nbgen.init_params(cfg) * 2.5)
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
     y = grid.label(cfg.kind, q)
     tau = m.calibrate(q, y)                       # global tau (allreduce min across ranks)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > the 126 MB L2
@@ -292,8 +325,39 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel ----------------
     fq = flop_per_query(cfg)
     peak, peak_src = load_peaks()
-    per_launch_ms = kernel_ms / max(1, launches)
-    achieved = fq * n / (per_launch_ms * 1e-3) / 1e12
+    calls = args.steps
+    per_launch_ms = kernel_ms / max(1, calls)
+    exit_info = None
+    if cfg.n_heads > 0:
+        fq_exec = executed_flop_per_query(cfg, c["exit_hist"], n)
+        achieved = fq_exec * n / (per_launch_ms * 1e-3) / 1e12
+        # the dense kernel (every head on every row) on the same model, same protocol
+        nb.lib().nb_debug_set_dense_exits(1)
+        for i in range(3):
+            step(i)
+        torch.cuda.synchronize()
+        dts = []
+        for i in range(min(args.steps, 10)):
+            flush.fill_(i & 0xFF)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            step(i)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            dts.append(a0.elapsed_time(a1))
+        nb.lib().nb_debug_set_dense_exits(0)
+        assert m.counts_dict(out[0]) == c
+        dense_ms = sorted(dts)[len(dts) // 2]
+        exit_info = {"exit_hist": c["exit_hist"], "bins": "exit@1, exit@2, final-negative, final-positive",
+                     "survive_head1": (n - c["exit_hist"][0]) / n,
+                     "survive_head2": (n - c["exit_hist"][0] - c["exit_hist"][1]) / n,
+                     "executed_flop_per_query": fq_exec, "dense_flop_per_query": fq,
+                     "dense_kernel_q_per_s": n * world / (dense_ms * 1e-3),
+                     "dense_kernel_ms_per_step": dense_ms,
+                     "model": f"trained {args.exit_train_steps} Adam steps (Eq. 1, alpha 1->1000) "
+                              "from Xavier init, calibrated to FN = 0 on the step's queries"}
+    else:
+        achieved = fq * n / (per_launch_ms * 1e-3) / 1e12
     traffic, tensor_pct = load_traffic()
     # ---------------- end to end: host buffers through the C ABI ----------------
     q_h = q.cpu().pin_memory()
@@ -331,7 +395,8 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": KERNEL[CONFIG], "flop_per_query": fq,
+                         "kernel": KERNEL[CONFIG],
+                         "flop_per_query": exit_info["executed_flop_per_query"] if exit_info else fq,
                          "kernel_ms_per_launch": per_launch_ms,
                          "ncu_tensor_pipe_pct": tensor_pct},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (4 * cfg.record_floats + 1),
@@ -343,6 +408,8 @@ def run_ours(args):
         }
         if train is not None:
             line["train"] = train
+        if exit_info is not None:
+            line["early_exit"] = exit_info
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_sample)
         print(json.dumps(line), flush=True)
@@ -408,6 +475,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 23)
     ap.add_argument("--train-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exit-train-steps", type=int, default=2000,
+                    help="c4: Adam steps before timing so the exit heads reject empty space")
     args = ap.parse_args()
     global CONFIG
     CONFIG = args.config

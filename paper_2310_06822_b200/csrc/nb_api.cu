@@ -174,7 +174,9 @@ static cudaError_t launch_forward_any(const nb_model* m, int mode, const FwdArgs
                                       cudaStream_t s) {
   timing_begin(m, s);
   if (mode == kScore && !g_dense_exits && exit_compaction_supported(m)) {
-    cudaError_t e = launch_score_exit(const_cast<nb_model*>(m), a, s);
+    int k = 0;
+    cudaError_t e = launch_score_exit(const_cast<nb_model*>(m), a, s, &k);
+    if (timing_on(m)) const_cast<nb_model*>(m)->kernel_launches += k - 1;  // + timing_end's one
     timing_end(m, s);
     return e;
   }
@@ -412,7 +414,7 @@ nb_status nb_model_kernel_time(nb_model* m, double* ms, int64_t* launches) {
     tot += t;
   }
   *ms = tot;
-  *launches = m->ev_used;
+  *launches = m->kernel_launches;  // kernels (an early-exit score is 3 per chunk)
   m->ev_used = 0;
   m->kernel_launches = 0;
   return NB_OK;

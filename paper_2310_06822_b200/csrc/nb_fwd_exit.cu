@@ -73,7 +73,7 @@ struct ExitSmem {
     uint32_t o = (wbytes + 127u) & ~127u;
     bars = o;  o += 8 * (1 + kXSlots + 2 * kXSlots);       // weights, acc_full[s], stage[s][2]
     tslot = o; o += 16;
-    xch = o;   o += 4 * kXSlots * 2 * 4 * 32 * 2;           // head partial of the other half
+    xch = o;   o += 4 * kXSlots * 2 * 4 * 32;               // head partial of the other half
     xpos = o;  o += 4 * kXSlots * 2 * 4 * 32;               // compacted position (or -1)
     qcnt = o;  o += 4 * kXSlots * 2 * 4;                    // survivors per row quarter
     ctr = o;   o += 4 * kXWarps * 12;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
     // combine the two column halves of each row
     float z = za + zb;
     {
-      float* xb = xch + (((s * 2 + par) * 4 + qw) * 32 + lane) * 2;
+      float* xb = xch + ((s * 2 + par) * 4 + qw) * 32 + lane;
       if (!lead) xb[0] = z;
       asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");
       if (lead) z += xb[0];
@@ -506,12 +506,17 @@ bool exit_compaction_supported(const nb_model* m) {
 // Score with early exits: per chunk of rows, segment 0 (records -> head 1),
 // segment 1 (image -> head 2), segment 2 (image -> output, classify).  All
 // launches add to a.counts; the last one finalises into a.fin_out.
-cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st) {
+static int64_t g_exit_chunk = 0;  // rows per chunk override (tests), 0 = default
+extern "C" void nb_debug_set_exit_chunk(int64_t rows) { g_exit_chunk = rows; }
+
+cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st, int* kernels) {
+  *kernels = 0;
   static const int64_t env_chunk = [] {
     const char* e = getenv("NB_EXIT_CHUNK");
-    return e ? std::max<int64_t>(kTile, atoll(e) / kTile * kTile) : (int64_t)1 << 22;
+    return e ? atoll(e) : (int64_t)1 << 24;
   }();
-  const int64_t chunk = std::min<int64_t>(env_chunk, (a.n + kTile - 1) / kTile * kTile);
+  const int64_t want = std::max<int64_t>(kTile, (g_exit_chunk > 0 ? g_exit_chunk : env_chunk) / kTile * kTile);
+  const int64_t chunk = std::min<int64_t>(want, (a.n + kTile - 1) / kTile * kTile);
   const int R = m->num_sms * kXSlots;
   const int64_t t0 = (chunk + kTile - 1) / kTile;
   const int64_t cap = (t0 + R + R - 1) / R;
@@ -551,6 +556,7 @@ cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st) {
     p.out_img = img[0]; p.out_lab = lab[0]; p.out_cnt = cnt[0];
     cudaError_t e = m->d0 == 4 ? launch_seg<2, false, 0, 4>(m, p, st) : launch_seg<2, false, 0, 0>(m, p, st);
     if (e != cudaSuccess) return e;
+    *kernels += 3;
     // segment 1: image -> layers [h0, h1) -> head 2
     p.lb = h0;
     p.tau_end = a.tau[2];

@@ -174,7 +174,7 @@ cudaError_t launch_fwd_simt(const nb_model* m, int mode, const FwdArgs& a, cudaS
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 bool exit_compaction_supported(const nb_model* m);
-cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t s);
+cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t s, int* kernels);
 bool tc_supported(const nb_desc& d);
 bool tc2_supported(const nb_desc& d);
 bool simt_supported(const nb_desc& d);

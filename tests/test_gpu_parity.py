@@ -1,6 +1,8 @@
 """GPU parity tests: the CUDA path through the C ABI against the oracle on the
 same seeded inputs (protocol P1-P6; tolerances from
 BASELINE.json north_star).  All marked gpu."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -625,17 +627,26 @@ def test_exit_compaction_counts_equal_dense(n):
 
 
 def test_exit_compaction_vs_oracle_and_chunks():
-    """Two compaction chunks (2^22 rows each by default) plus a ragged tail:
-    counts equal the bf16-emulating oracle's outside the 1e-3 band of every
-    threshold (R28), and equal the dense kernel's everywhere."""
+    """Compaction in chunks (2^20 rows here, so four chunks plus a ragged
+    tail; 2^24 by default): counts equal the dense kernel's and the
+    bf16-emulating oracle's outside the 1e-3 band of every threshold
+    (R28)."""
     n = (1 << 22) + 3 * 128 + 11
     cfg, q, y, m = _exit_model(n, seed=1)
     qd, yd = cuda(q), cuda(y)
     z = m.forward(qd).cpu()
     tau = [float(z[:, 0].median()), float(z[:, 1].quantile(0.5)), float(z[:, 2].quantile(0.2))]
     m.set_thresholds(tau)
-    c, d = _score_both(m, qd, yd)
-    assert c == d
+    L = nb.lib()
+    L.nb_debug_set_exit_chunk.argtypes = [ctypes.c_int64]
+    try:
+        L.nb_debug_set_exit_chunk(1 << 20)
+        c, d = _score_both(m, qd, yd)
+        L.nb_debug_set_exit_chunk(0)
+        c1, _ = _score_both(m, qd, yd)
+    finally:
+        L.nb_debug_set_exit_chunk(0)
+    assert c == d and c1 == d
     # oracle on a sample of rows away from every threshold
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(n, 40000, replace=False))
