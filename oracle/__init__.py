@@ -37,7 +37,8 @@ def build(force: bool = False) -> str:
 
 class Arch(C.Structure):
     _fields_ = [("d0", C.c_int32), ("width", C.c_int32), ("layers", C.c_int32),
-                ("n_heads", C.c_int32), ("head_after", C.c_int32 * 2)]
+                ("n_heads", C.c_int32), ("head_after", C.c_int32 * 2),
+                ("act", C.c_int32), ("pe", C.c_int32)]
 
 
 class Counts(C.Structure):
@@ -98,19 +99,28 @@ def _np(x, dtype):
     return np.ascontiguousarray(x, dtype=dtype)
 
 
+ACT = {"relu": 0, "sine": 1}
+
+
 def arch_of(cfg) -> Arch:
     a = Arch()
     a.d0, a.width, a.layers, a.n_heads = cfg.record_floats, cfg.width, cfg.hidden_layers, cfg.n_heads
     for k, l in enumerate(cfg.head_after):
         a.head_after[k] = l
+    a.act = ACT[getattr(cfg, "activation", "relu")]
+    a.pe = getattr(cfg, "pe_depth", 0)
     return a
 
 
-def make_arch(d0, width, layers, head_after=()) -> Arch:
+def make_arch(d0, width, layers, head_after=(), act="relu", pe=0) -> Arch:
+    """d0 = record floats; act "relu" | "sine" (R1, R41); pe = positional
+    encoding depth (R42), layer 1 then reads d0 (1 + pe) inputs."""
     a = Arch()
     a.d0, a.width, a.layers, a.n_heads = d0, width, layers, len(head_after)
     for k, l in enumerate(head_after):
         a.head_after[k] = l
+    a.act = ACT[act]
+    a.pe = pe
     return a
 
 

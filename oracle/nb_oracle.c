@@ -315,13 +315,35 @@ void ora_encode_bf16(const float* q, int64_t n, int32_t d0, uint16_t* out) {
 }
 
 /* ------------------------------------------------------------------------ */
-/* MLP h_theta (§3.4): h_0 = x; z_l = W_l h_{l-1} + b_l;
- * h_l = ReLU(z_l) (R1); z = w_out . h_L + b_out; yhat = sigmoid(z).
+/* Input of layer 1 (Suppl. §3, NeRF positional encoding; R42):
+ * gamma(x) = (x_1..x_r, then for k = 0 .. L/2-1: sin(2^k pi x_1..r),
+ * cos(2^k pi x_1..r)), L = pe; "2D point * 8 encodings, plus the 2D input"
+ * = 18 values for r = 2, L = 8.  pe = 0: the record itself.              */
+static int input_dim(const ora_arch* a) { return a->d0 * (1 + a->pe); }
+
+static void positional_encoding(const ora_arch* a, const float* r, double* f) {
+  const int d = a->d0;
+  for (int j = 0; j < d; ++j) f[j] = (double)r[j];
+  for (int k = 0; k < a->pe / 2; ++k)
+    for (int j = 0; j < d; ++j) {
+      const double u = ldexp(3.14159265358979323846, k) * (double)r[j];
+      f[d + 2 * k * d + j] = sin(u);
+      f[d + (2 * k + 1) * d + j] = cos(u);
+    }
+}
+
+/* Hidden activation sigma and its derivative: ReLU (R1, R25: ReLU'(0) = 0) or
+ * sine with frequency 1 ("Sinusoidal activations"; R41).            */
+static double act_fn(const ora_arch* a, double z) { return a->act ? sin(z) : (z > 0.0 ? z : 0.0); }
+static double act_grad(const ora_arch* a, double z) { return a->act ? cos(z) : (z > 0.0 ? 1.0 : 0.0); }
+
+/* MLP h_theta (§3.4): h_0 = gamma(x); z_l = W_l h_{l-1} + b_l;
+ * h_l = sigma(z_l); z = w_out . h_L + b_out; yhat = sigmoid(z).
  * Exit heads (§3.3, R22): e_k = u_k . h_{l_k} + c_k.
  * Canonical parameter blob (R32): per hidden layer W_l[out][in] then b_l;
  * then w_out[w], b_out; then per head u_k[w], c_k.                       */
 int64_t ora_num_params(const ora_arch* a) {
-  int64_t n = 0, in = a->d0;
+  int64_t n = 0, in = input_dim(a);
   for (int l = 0; l < a->layers; ++l) {
     n += (in + 1) * (int64_t)a->width;
     in = a->width;
@@ -334,7 +356,7 @@ int64_t ora_num_params(const ora_arch* a) {
 typedef struct { int64_t W[16], b[16], wout, bout, u[2], c[2]; } offsets;
 
 static void param_offsets(const ora_arch* a, offsets* o) {
-  int64_t p = 0, in = a->d0;
+  int64_t p = 0, in = input_dim(a);
   for (int l = 0; l < a->layers; ++l) {
     o->W[l] = p; p += in * a->width;
     o->b[l] = p; p += a->width;
@@ -355,22 +377,22 @@ static int head_at(const ora_arch* a, int l1) { /* head index reading hidden lay
 }
 
 /* One query forward.  acts (optional, fp64 mode): h_0..h_L stored as
- * [L+1][max(d0,w)] and pre-activations z_1..z_L as [L][w].               */
+ * [L+1][max(d_in,w)] and pre-activations z_1..z_L as [L][w].             */
 static void forward_one(const ora_arch* a, const offsets* of, const double* th, const float* r,
                         int mode, double* out, double* acts, double* pre) {
-  const int w = a->width, L = a->layers, d0 = a->d0;
+  const int w = a->width, L = a->layers, d0 = input_dim(a);
   const int stride = (d0 > w ? d0 : w);
   double hbuf[2][512];
   double* h = hbuf[0];
   double* hn = hbuf[1];
-  if (mode == ORA_BF16_EMU) {
+  positional_encoding(a, r, h);
+  if (mode == ORA_BF16_EMU) {  /* fp32 feature -> bf16 (hi, lo) pair (R20) */
     for (int j = 0; j < d0; ++j) {
-      float hi = bf16_round(r[j]);
-      float lo = bf16_round(r[j] - hi);
+      float x = (float)h[j];
+      float hi = bf16_round(x);
+      float lo = bf16_round(x - hi);
       h[j] = (double)hi + (double)lo;
     }
-  } else {
-    for (int j = 0; j < d0; ++j) h[j] = (double)r[j];
   }
   if (acts) for (int j = 0; j < d0; ++j) acts[j] = h[j];
   int in = d0;
@@ -387,14 +409,14 @@ static void forward_one(const ora_arch* a, const offsets* of, const double* th, 
       }
       if (mode == ORA_BF16_EMU) {
         float z = (float)s + (float)b[o];
-        float rr = z > 0.0f ? z : 0.0f;
+        float rr = (float)act_fn(a, (double)z);
         if (pre) pre[(int64_t)l * w + o] = (double)z;
         rl[o] = rr;
         hn[o] = (l < L - 1) ? (double)bf16_round(rr) : (double)rr;
       } else {
         double z = s + b[o];
         if (pre) pre[(int64_t)l * w + o] = z;
-        rl[o] = z > 0.0 ? z : 0.0;
+        rl[o] = act_fn(a, z);
         hn[o] = rl[o];
       }
     }
@@ -424,7 +446,7 @@ void ora_forward(const ora_arch* a, const double* theta, const float* q, int64_t
   const int nl = 1 + a->n_heads;
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i)
-    forward_one(a, &of, theta, q + i * a->d0, mode, logits + i * nl, NULL, NULL);
+    forward_one(a, &of, theta, q + i * a->d0, mode, logits + i * nl, NULL, NULL); /* d0 = record */
 }
 
 /* ------------------------------------------------------------------------ */
@@ -446,7 +468,7 @@ static double loss_grad_impl(const ora_arch* a, const double* th, const float* q
                              double beta, double* grad, ora_stats* st, int mode) {
   offsets of;
   param_offsets(a, &of);
-  const int w = a->width, L = a->layers, d0 = a->d0;
+  const int w = a->width, L = a->layers, d0 = input_dim(a);
   const int stride = (d0 > w ? d0 : w);
   const int64_t P = ora_num_params(a);
   memset(grad, 0, sizeof(double) * P);
@@ -459,7 +481,7 @@ static double loss_grad_impl(const ora_arch* a, const double* th, const float* q
   const double B = (double)n_global;
   for (int64_t i = 0; i < n; ++i) {
     double out[3];
-    forward_one(a, &of, th, q + i * d0, mode, out, acts, pre);
+    forward_one(a, &of, th, q + (int64_t)i * a->d0, mode, out, acts, pre);
     const int yi = y[i] ? 1 : 0;
     const double wi = yi ? alpha : beta;
     /* output logit and its gradient dL/dz = w (sigmoid(z) - y) / B (a7) */
@@ -489,7 +511,7 @@ static double loss_grad_impl(const ora_arch* a, const double* th, const float* q
         }
         grad[of.c[k]] += ge[k];
       }
-      for (int o = 0; o < w; ++o) dz[o] = pre[(int64_t)l * w + o] > 0.0 ? dh[o] : 0.0; /* R25 */
+      for (int o = 0; o < w; ++o) dz[o] = dh[o] * act_grad(a, pre[(int64_t)l * w + o]); /* R25, R41 */
       const int in = (l == 0) ? d0 : w;
       const double* hin = acts + (int64_t)l * stride;
       const double* W = th + of.W[l];

@@ -33,6 +33,8 @@ typedef struct {
   int32_t layers;        /* hidden layers L                               */
   int32_t n_heads;       /* early-exit heads (0..2), §3.3       */
   int32_t head_after[2]; /* 1-based hidden layer each head reads          */
+  int32_t act;           /* 0 ReLU (BJ, R1); 1 sine h = sin(z) (R41) */
+  int32_t pe;            /* positional-encoding depth L (Suppl. §3, R42) */
 } ora_arch;
 
 typedef struct { uint64_t tp, fp, fn, tn, exit_hist[4], nonfinite; } ora_counts;
