@@ -68,9 +68,20 @@ typedef enum { NB_POINT = 0, NB_RAY = 1, NB_PLANE = 2, NB_BOX = 3 } nb_query_kin
  *          (configs[1..4]); inputs enter as a bf16 (hi, lo) pair (R20). */
 typedef enum { NB_FP32 = 0, NB_BF16 = 1 } nb_precision;
 
-/* MLP architecture (§3.4; Suppl. Tab. 4): d0 -> width x hidden_layers -> 1,
- * ReLU hidden activations (R1), optional early-exit heads reading hidden
- * layers head_after[k] (1-based; §3.3, R22). */
+/* Hidden activation: ReLU (BASELINE.json, R1) or the paper's sine
+ * ("Sinusoidal activations are used in the hidden layers"; h = sin(z),
+ * frequency 1, R41). */
+typedef enum { NB_RELU = 0, NB_SINE = 1 } nb_activation;
+
+/* MLP architecture (§3.4; Suppl. Tab. 4): d_in -> width x hidden_layers -> 1,
+ * optional early-exit heads reading hidden layers head_after[k] (1-based;
+ * P:231-279 §3.3, R22).  d_in = r (1 + pe_depth) for r record floats:
+ * pe_depth = 0 feeds the record itself; an even pe_depth = L > 0 applies the
+ * NeRF positional encoding of Suppl. §3 (R42)
+ *   gamma(x) = (x, sin(2^0 pi x), cos(2^0 pi x), ..., sin(2^(L/2-1) pi x), cos(...))
+ * ordered as [x_1..x_r, then per frequency k: sin(2^k pi x_1..r), cos(2^k pi x_1..r)]
+ * (2D points with L = 8 give the paper's 18 inputs).  Zero-initialised
+ * activation / pe_depth mean ReLU without encoding. */
 typedef struct {
   int32_t kind;          /* nb_query_kind                                    */
   int32_t space_dim;     /* 2, 3 or 4 (4 = 3D + time, points only)          */
@@ -79,6 +90,8 @@ typedef struct {
   int32_t n_heads;       /* 0..2 early-exit heads                            */
   int32_t head_after[2]; /* 1-based hidden layer read by each head           */
   int32_t precision;     /* nb_precision                                     */
+  int32_t activation;    /* nb_activation (0 = ReLU)                         */
+  int32_t pe_depth;      /* 0, or even L in 2..16 (positional encoding)      */
 } nb_desc;
 
 /* Confusion counts of the calibrated predictor (P:157-176 cost cases);
@@ -152,7 +165,8 @@ nb_status nb_comm_version(int32_t* version);
 /* a1 encoder (R20).  NB_BF16: x_out is uint16 [n][16] bf16 bit
  * patterns (hi(0..d0-1), lo(0..d0-1), zeros); NB_FP32: x_out is fp32 [n][d0]
  * (identity).  The compute calls below encode in-kernel; this exposes the exact
- * layer-1 operand for parity.                                                 */
+ * layer-1 operand for parity.  Models with pe_depth > 0 return
+ * NB_E_UNSUPPORTED (their encoding runs inside the kernels only).            */
 nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream);
 
 /* a1-a4: logits[n][1 + n_heads] (output logit z, then head logits e_k), fp32;

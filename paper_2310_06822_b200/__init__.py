@@ -27,6 +27,7 @@ POINT, RAY, PLANE, BOX = 0, 1, 2, 3
 KINDS = {"point": POINT, "ray": RAY, "plane": PLANE, "box": BOX}
 FP32, BF16 = 0, 1
 PRECISIONS = {"fp32": FP32, "bf16": BF16}
+ACTIVATIONS = {"relu": 0, "sine": 1}  # nb_activation (R1, R41)
 STATUS = ["NB_OK", "NB_E_ARG", "NB_E_SHAPE", "NB_E_NONFINITE", "NB_E_LABEL",
           "NB_E_NO_POSITIVES", "NB_E_CUDA", "NB_E_NCCL", "NB_E_UNSUPPORTED", "NB_E_OOM"]
 NB_OK, NB_E_NONFINITE, NB_E_NO_POSITIVES = 0, 3, 5
@@ -42,7 +43,8 @@ class NBError(RuntimeError):
 class _Desc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("space_dim", C.c_int32), ("width", C.c_int32),
                 ("hidden_layers", C.c_int32), ("n_heads", C.c_int32),
-                ("head_after", C.c_int32 * 2), ("precision", C.c_int32)]
+                ("head_after", C.c_int32 * 2), ("precision", C.c_int32),
+                ("activation", C.c_int32), ("pe_depth", C.c_int32)]
 
 
 class _Counts(C.Structure):
@@ -168,6 +170,8 @@ class Desc:
     hidden_layers: int = 4
     head_after: tuple = ()
     precision: str = "bf16"
+    activation: str = "relu"   # or "sine" (R41)
+    pe_depth: int = 0          # positional encoding depth L (Suppl. §3, R42)
 
     def to_c(self) -> _Desc:
         d = _Desc()
@@ -179,6 +183,8 @@ class Desc:
         for k, l in enumerate(self.head_after):
             d.head_after[k] = l
         d.precision = PRECISIONS[self.precision]
+        d.activation = ACTIVATIONS[self.activation]
+        d.pe_depth = self.pe_depth
         return d
 
     @property

@@ -47,14 +47,22 @@ static bool desc_valid(const nb_desc* d, int* d0_out) {
     if (d->head_after[k] < 1 || d->head_after[k] > d->hidden_layers) return false;
   if (d->n_heads == 2 && d->head_after[0] >= d->head_after[1]) return false;
   if (d->precision != NB_FP32 && d->precision != NB_BF16) return false;
+  if (d->activation != NB_RELU && d->activation != NB_SINE) return false;
+  if (d->pe_depth < 0 || d->pe_depth > 16 || (d->pe_depth & 1)) return false;
   int d0 = d->kind == NB_POINT ? d->space_dim : 2 * d->space_dim;
   if (d0 > 8) return false;
   if (d0_out) *d0_out = d0;
   return true;
 }
 
-static void param_offsets(const nb_desc& d, int d0, ParamOffsets* o) {
-  int64_t p = 0, in = d0;
+// Layer-1 input features: the record, or its positional encoding (R42).
+static int input_features(const nb_desc& d) {
+  const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
+  return r * (1 + d.pe_depth);
+}
+
+static void param_offsets(const nb_desc& d, int din, ParamOffsets* o) {
+  int64_t p = 0, in = din;
   for (int l = 0; l < d.hidden_layers; ++l) {
     o->W[l] = p; p += in * d.width;
     o->b[l] = p; p += d.width;
@@ -81,8 +89,10 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   const uint32_t W = (uint32_t)d.width;
   pl->pairs = (d.precision == NB_BF16 && W > 128) ? 2u : 1u;
   const uint32_t rows = W / pl->pairs;
+  const int din = input_features(d);
+  const uint32_t K0 = enc_k(din);
   for (int l = 0; l < d.hidden_layers; ++l) {
-    const uint32_t K = l == 0 ? (uint32_t)kEncK : W;
+    const uint32_t K = l == 0 ? K0 : W;
     pl->off_w[l] = off;
     pl->k_of[l] = K;
     off = align_up(off + rows * K * 2u, 128u);
@@ -97,10 +107,9 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   pl->off_c = off; off += 16u;
   off = align_up(off, 128u);
   pl->core_bytes = off;
-  const int d0 = (int)nb_record_floats(d.kind, d.space_dim);
   const bool shared = pl->pairs == 2 && d.precision == NB_BF16 && 3 * (d.hidden_layers - 1) <= kEncK;
   const bool fold = (pl->pairs == 1 && d.precision == NB_BF16) || shared;
-  pl->bias_l0 = (fold && 2 * d0 + 3 <= kEncK) ? 1u : 0u;
+  pl->bias_l0 = (fold && 2 * din + 3 <= (int)K0) ? 1u : 0u;
   pl->bb_shared = shared ? 1u : 0u;
   for (int l = 0; l < kMaxLayers; ++l) pl->off_bb[l] = 0;
   if (shared) {
@@ -213,9 +222,8 @@ int64_t nb_record_floats(int32_t kind, int32_t space_dim) {
 }
 
 int64_t nb_num_params(const nb_desc* d) {
-  int d0;
-  if (!desc_valid(d, &d0)) return -1;
-  int64_t n = 0, in = d0;
+  if (!desc_valid(d, nullptr)) return -1;
+  int64_t n = 0, in = input_features(*d);
   for (int l = 0; l < d->hidden_layers; ++l) {
     n += (in + 1) * (int64_t)d->width;
     in = d->width;
@@ -274,8 +282,9 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   for (int k = desc->n_heads; k < 2; ++k) m->d.head_after[k] = 0;
   m->device = device;
   m->d0 = d0;
+  m->din = input_features(*desc);
   m->P = nb_num_params(desc);
-  param_offsets(m->d, d0, &m->po);
+  param_offsets(m->d, m->din, &m->po);
   pack_layout(m->d, &m->pl);
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaSuccess;
@@ -457,6 +466,9 @@ nb_status nb_model_get_thresholds(const nb_model* m, float* tau, int32_t n) {
 
 nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream) {
   if (!m || n < 0 || (n > 0 && (!q || !x_out))) return set_error("bad argument"), NB_E_ARG;
+  if (m->d.pe_depth > 0)  // the kernels encode in place; no materialised PE operand yet
+    return set_error("nb_encode: positional encoding is applied inside the kernels only"),
+           NB_E_UNSUPPORTED;
   DeviceGuard g(m->device);
   NB_CUDA(launch_encode(m, q, n, x_out, (cudaStream_t)stream));
   return NB_OK;
@@ -674,18 +686,17 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = m->d.precision == NB_BF16;
   if (tc && !train_tc_supported(m->d)) {
-    set_error("bf16 training not built for width %d", m->d.width);
+    set_error("bf16 training not built for width %d / sine / positional encoding", m->d.width);
     return NB_E_UNSUPPORTED;
   }
-  if (!tc && m->d.width > 32) {
-    set_error("fp32 training supports width <= 32");
+  if (!tc && (m->d.width > 32 || m->din > m->d.width)) {
+    set_error("fp32 training supports width <= 32 and input features <= width");
     return NB_E_UNSUPPORTED;
   }
   size_t need = tc ? train_tc_scratch_bytes(m, n_local) : train_simt_scratch_bytes(m, n_local);
   if (need > m->train_scratch_bytes) {
     NB_CUDA(cudaStreamSynchronize(s));
     cudaFree(m->train_scratch);
-  cudaFree(m->exit_scratch);
     m->train_scratch = nullptr;
     m->train_scratch_bytes = 0;
     cudaError_t e = cudaMalloc(&m->train_scratch, need);

@@ -8,7 +8,10 @@ bool tc_supported(const nb_desc& d) {
   if (d.precision != NB_BF16) return false;
   if (!(d.width == 32 || d.width == 64 || d.width == 128)) return false;
   if (d.hidden_layers < 1 || d.hidden_layers > kMaxLayers) return false;
-  return true;
+  // layer-1 operand (hi, lo and bias columns) fits the slot's A region
+  const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
+  const int k0 = enc_k(r * (1 + d.pe_depth));
+  return k0 <= kTcMaxEncK && k0 <= d.width;
 }
 
 // NB_TRACE builds: device buffer set by nb_debug_set_trace (tools/trace_fwd.py).
@@ -26,11 +29,12 @@ cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStr
   const nb_desc& d = m->d;
   const int h0 = d.n_heads > 0 ? d.head_after[0] : 0, h1 = d.n_heads > 1 ? d.head_after[1] : 0;
   const bool bf = m->pl.bias_l0 != 0;
-  if (bf && d.width == 64 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 3)
+  const bool plain = d.activation == NB_RELU && d.pe_depth == 0;  // specialised kernels: ReLU, no PE
+  if (bf && plain && d.width == 64 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 3)
     return launch_tc_w64l4_d3(m, mode, a, st, !g_no_fold);
-  if (bf && d.width == 128 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 6)
+  if (bf && plain && d.width == 128 && d.hidden_layers == 4 && d.n_heads == 0 && m->d0 == 6)
     return launch_tc_w128l4_d6(m, mode, a, st, !g_no_fold);
-  if (bf && d.width == 128 && d.hidden_layers == 6 && h0 == 2 && h1 == 4 && m->d0 == 4)
+  if (bf && plain && d.width == 128 && d.hidden_layers == 6 && h0 == 2 && h1 == 4 && m->d0 == 4)
     return launch_tc_w128l6h24_d4(m, mode, a, st, !g_no_fold);
   const bool fold = bf && !g_no_fold;
   switch (d.width) {

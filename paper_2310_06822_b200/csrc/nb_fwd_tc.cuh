@@ -35,6 +35,7 @@ struct TcParams {
   const uint8_t* packed;
   PackLayout pl;
   int d0, L, nh, ha0, ha1;
+  int act, pe, din, k0;  // generic kernels: nb_activation, PE depth, layer-1 inputs and K (R41, R42)
   int64_t num_tiles;
   unsigned long long* trace;  // NB_TRACE builds only: timeline of CTA 0
 };
@@ -94,6 +95,42 @@ __device__ __forceinline__ void encode_cols(const float* x, int d0_rt, uint32_t 
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) col[c] = e[2 * c] | (e[2 * c + 1] << 16);
+}
+
+// a1 encode with positional encoding (generic kernels, R42): the
+// d_in = d0 (1 + pe) features [x, sin(2^k pi x), cos(2^k pi x) per frequency]
+// of one record, each split into a bf16 (hi, lo) pair, then three 1.0 bias
+// columns; K0 / 2 packed 32-bit columns (K0 = enc_k(d_in) <= 64).
+__device__ __forceinline__ void encode_cols_pe(const float* x, int d0, int pe, int k0, uint32_t (&col)[32]) {
+  float f[kTcMaxEncK / 2];
+  const int din = d0 * (1 + pe);
+  for (int j = 0; j < d0; ++j) f[j] = x[j];
+  for (int k = 0; k < pe / 2; ++k)
+    for (int j = 0; j < d0; ++j) {
+      float sv, cv;
+      sincospif(ldexpf(x[j], k), &sv, &cv);
+      f[d0 + 2 * k * d0 + j] = sv;
+      f[d0 + (2 * k + 1) * d0 + j] = cv;
+    }
+  auto elem = [&](int k) -> uint32_t {
+    if (k < din) return __bfloat16_as_ushort(__float2bfloat16_rn(f[k]));
+    if (k < 2 * din) {
+      const float v = f[k - din];
+      return __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(__float2bfloat16_rn(v))));
+    }
+    return k < 2 * din + 3 ? 0x3F80u : 0u;
+  };
+  for (int c = 0; c < 32; ++c) col[c] = 2 * c < k0 ? (elem(2 * c) | (elem(2 * c + 1) << 16)) : 0u;
+}
+
+// sine hidden activation (R41): 2 pi range reduction in fp32
+// (two-constant Cody-Waite), then the SFU sine on [-pi, pi]: |error| ~ 1e-6,
+// far below the bf16 rounding of the result
+__device__ __forceinline__ float sin_act(float x) {
+  const float k = rintf(x * 0.159154943091895336f);
+  float r = fmaf(-k, 6.28318548202514648f, x);
+  r = fmaf(-k, -1.74845553e-7f, r);
+  return __sinf(r);
 }
 
 __device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
@@ -220,7 +257,10 @@ struct TcPlan<128> { static constexpr int NSLOT = 2, WPS = 8, COLS = 512; };
 // a constant ones block in TMEM and whose B holds the exact bf16 split of b_l
 // (PackLayout::off_bb).  The epilogue of a hidden layer is then just
 // tcgen05.ld -> cvt.rn.relu.bf16x2 -> tcgen05.st.  D0C: compile-time d0.
-template <int W, int LC, int H0C, int H1C, int MODE, int D0C, bool BF>
+// EXT: generic kernels of sine / positional-encoding nets (run-time p.act,
+// p.pe; R41, R42) — kept apart so the ReLU kernels' register
+// allocation is unaffected.
+template <int W, int LC, int H0C, int H1C, int MODE, int D0C, bool BF, bool EXT = false>
 __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     k_fwd_tc(const TcParams p) {
   const int L = LC ? LC : p.L;
@@ -288,7 +328,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   for (int i = threadIdx.x; i < NEPI * 12; i += blockDim.x) ctr[i] = 0u;
   if (threadIdx.x < kMaxLayers) {
     const int l = threadIdx.x;
-    dtab[l] = make_sdesc(sbase + p.pl.off_w[l], 128u, (l == 0 ? kEncK / 8u : W / 8u) * 128u);
+    dtab[l] = make_sdesc(sbase + p.pl.off_w[l], 128u, (l == 0 ? p.pl.k_of[0] / 8u : W / 8u) * 128u);
     dtab[kMaxLayers + l] = make_sdesc(sbase + p.pl.off_bb[l], 128u, (kEncK / 8u) * 128u);
   }
   tc_fence_before();
@@ -350,6 +390,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         const uint32_t a = tmem + a_col(s);
         if (l == 0) {
           mma_ts(d, a, dtab[0], idesc, 0u);
+          if (EXT)  // positional encoding: K0 = 32 .. 64
+            for (uint32_t kk = 1; kk < (uint32_t)p.k0 / 16u; ++kk)
+              mma_ts(d, a + kk * 8u, dtab[0] + (uint64_t)(kk * 16u), idesc, 1u);
         } else {
           if (BF)  // bias first: D = ones * [hi mid lo]^T, then D += A W^T
             mma_ts(d, tmem + kOnesCol, dtab[kMaxLayers + l], idesc, 0u);
@@ -399,15 +442,22 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
         ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
       }
-      uint32_t c[8];
-      encode_cols<D0C, BF>(x, d0, c);
-      tmem_st8(trow + a_col(s), c);
-      if (MODE == kTrain) {  // layer-1 input image for the dW GEMM
-        uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(16);
+      if (EXT && p.pe > 0) {
+        uint32_t c[32];
+        encode_cols_pe(x, d0, p.pe, p.k0, c);
+        for (int g = 0; g < p.k0 / 16; ++g)
+          tmem_st8(trow + a_col(s) + (uint32_t)(8 * g), *reinterpret_cast<const uint32_t(*)[8]>(c + 8 * g));
+      } else {
+        uint32_t c[8];
+        encode_cols<D0C, BF>(x, d0, c);
+        tmem_st8(trow + a_col(s), c);
+        if (MODE == kTrain) {  // layer-1 input image for the dW GEMM (ReLU, no PE)
+          uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(16);
 #pragma unroll
-        for (int fg = 0; fg < 2; ++fg)
-          *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
-              make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+          for (int fg = 0; fg < 2; ++fg)
+            *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+        }
       }
       tmem_wait_st();
     }
@@ -472,8 +522,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         }
         if (!last || MODE == kTrain) {
           uint32_t pk[16];
+          if (EXT && p.act == NB_SINE) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+            for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(sin_act(t[2 * j]), sin_act(t[2 * j + 1]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+          }
           if (!last) tmem_st16(trow + a_col(s) + (uint32_t)((col0 + 32 * c) / 2), pk);
           if (MODE == kTrain) {  // h_{l+1} image (activations kept for back-propagation)
             uint8_t* base = p.a.tr.h_img[l] + tile * img_tile_bytes(W);
@@ -485,8 +540,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           }
         }
         if (l == h0 || l == h1 || last) {
+          if (EXT && p.act == NB_SINE) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) t[i] = relu_nan(t[i]);
+            for (int i = 0; i < 32; ++i) t[i] = sin_act(t[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) t[i] = relu_nan(t[i]);
+          }
           const int o = 32 * c;
           // head vectors: 16-B aligned (pack layout, col0 % 32 == 0) -> LDS.128
           auto dot = [&](float& sa, float& sb, const float* w) {
@@ -597,7 +657,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
 // Trace buffer of NB_TRACE builds (defined in nb_fwd_tc.cu).
 extern unsigned long long* g_trace_buffer;
 
-template <int W, int LC, int H0C, int H1C, int MODE, int D0C, bool BF>
+template <int W, int LC, int H0C, int H1C, int MODE, int D0C, bool BF, bool EXT = false>
 inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
   constexpr int NSLOT = TcPlan<W>::NSLOT, WPS = TcPlan<W>::WPS;
   TcParams p;
@@ -609,6 +669,10 @@ inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   p.nh = m->d.n_heads;
   p.ha0 = m->d.head_after[0];
   p.ha1 = m->d.head_after[1];
+  p.act = m->d.activation;
+  p.pe = m->d.pe_depth;
+  p.din = m->din;
+  p.k0 = (int)m->pl.k_of[0];
   p.num_tiles = (a.n + kTile - 1) / kTile;
   p.trace = g_trace_buffer;
   if (p.num_tiles == 0) return cudaSuccess;
@@ -620,12 +684,21 @@ inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
                 sizeof(float) * NSLOT * 2 * 4 * 32 * 3 + 4 * NSLOT * WPS * 12 + 8 * 2 * NSLOT +
                 sizeof(float) * NSLOT * 2 * kTile * 8 + NSLOT * 2 * kTile + 16 * 8;
   smem = std::max<size_t>(smem, 116 * 1024);
-  auto kern = k_fwd_tc<W, LC, H0C, H1C, MODE, D0C, BF>;
+  auto kern = k_fwd_tc<W, LC, H0C, H1C, MODE, D0C, BF, EXT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
   kern<<<grid, NSLOT * WPS * 32, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+// Generic sine / PE kernels (bias folded; forward, calibrate, score).
+template <int W>
+inline cudaError_t launch_tc_ext(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (mode == kForward) return launch_tc_wm<W, 0, 0, 0, kForward, 0, true, true>(m, a, st);
+  if (mode == kCalibrate) return launch_tc_wm<W, 0, 0, 0, kCalibrate, 0, true, true>(m, a, st);
+  if (mode == kScore) return launch_tc_wm<W, 0, 0, 0, kScore, 0, true, true>(m, a, st);
+  return cudaErrorInvalidValue;
 }
 
 template <int W, int LC, int H0C, int H1C, int D0C, bool BF>

@@ -451,7 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
 
 bool tc2_supported(const nb_desc& d) {
   return d.precision == NB_BF16 && d.width == 256 && d.hidden_layers >= 1 &&
-         d.hidden_layers <= kMaxLayers;
+         d.hidden_layers <= kMaxLayers && d.activation == NB_RELU && d.pe_depth == 0;
 }
 
 template <int LC, int MODE, bool BF>

@@ -14,7 +14,12 @@ namespace nb {
 
 constexpr int kMaxLayers = 8;
 constexpr int kTile = 128;          // rows per MMA tile (M = 128)
-constexpr int kEncK = 16;           // layer-1 K after the bf16 (hi, lo) split
+constexpr int kEncK = 16;           // layer-1 K after the bf16 (hi, lo) split (no encoding)
+// layer-1 K for d_in input features: hi and lo halves plus three bias ones
+// columns, rounded up to the MMA K step (16 for every record without PE)
+__host__ __device__ constexpr int enc_k(int din) { return (2 * din + 3 + 15) / 16 * 16; }
+constexpr int kSimtMaxIn = 64;      // fp32 path: layer-1 input features (with PE)
+constexpr int kTcMaxEncK = 64;      // bf16 path: layer-1 K (2 d_in + 3 <= 64)
 constexpr int kNumCounters = 9;     // tp fp fn tn exit[4] nonfinite
 constexpr int kCtrStride = 16;      // device counters 128 B apart (one L2 line each); set 1 at +8
 constexpr int kFinOff = kNumCounters * kCtrStride;  // nb_model::d_counts: finalised totals
@@ -70,7 +75,8 @@ struct ParamOffsets {  // canonical fp32 blob offsets (nb.h nb_num_params)
 struct nb_model {
   nb_desc d;
   int device = 0;
-  int d0 = 0;
+  int d0 = 0;                 // record floats (query stride)
+  int din = 0;                // layer-1 input features: d0, or d0 (1 + pe_depth) (R42)
   int64_t P = 0;
   int num_sms = 0;
   nb::ParamOffsets po;

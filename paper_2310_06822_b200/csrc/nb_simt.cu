@@ -178,7 +178,7 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s) {
   a.po = m->po;
   a.W = m->d.width;
   a.L = m->d.hidden_layers;
-  a.d0 = m->d0;
+  a.d0 = m->din;  // layer-1 input features (hi columns [0, din), lo [din, 2 din))
   a.nh = m->d.n_heads;
   k_pack_bf16<<<148, 256, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
@@ -199,7 +199,27 @@ cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s) {
 struct SimtArgs {
   ParamOffsets po;
   int P, d0, L, nh, ha0, ha1;
+  int din, act, pe;  // layer-1 inputs, nb_activation, positional-encoding depth
 };
+
+// Layer-1 input of one record (R42): the record itself, then for
+// each frequency 2^k pi (k < pe / 2) sin and cos of every coordinate.
+// sincospif reduces 2^k x exactly (the scaling by a power of two is exact).
+__device__ __forceinline__ void simt_features(const float* x, int d0, int pe, float* f) {
+  for (int j = 0; j < d0; ++j) f[j] = x[j];
+  for (int k = 0; k < pe / 2; ++k)
+    for (int j = 0; j < d0; ++j) {
+      float sv, cv;
+      sincospif(ldexpf(x[j], k), &sv, &cv);
+      f[d0 + 2 * k * d0 + j] = sv;
+      f[d0 + (2 * k + 1) * d0 + j] = cv;
+    }
+}
+// hidden activation (R1 ReLU, R41 sine) and its derivative at z
+__device__ __forceinline__ float simt_act(float z, int act) { return act == NB_SINE ? sinf(z) : fmaxf(z, 0.f); }
+__device__ __forceinline__ float simt_dact(float z, int act) {
+  return act == NB_SINE ? cosf(z) : (z > 0.f ? 1.f : 0.f);  // ReLU'(0) = 0 (R25)
+}
 
 template <int W, int MODE>
 __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ theta, SimtArgs s,
@@ -226,11 +246,22 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
       for (int j = 0; j < 8; ++j) bad = bad || (j < s.d0 && !isfinite(x[j]));
       const float* W0 = sp + s.po.W[0];
       const float* b0 = sp + s.po.b[0];
+      if (s.pe == 0) {
 #pragma unroll
-      for (int o = 0; o < W; ++o) {
-        float acc_o = b0[o];
-        for (int k = 0; k < s.d0; ++k) acc_o = fmaf(W0[o * s.d0 + k], x[k], acc_o);
-        h[o] = fmaxf(acc_o, 0.f);
+        for (int o = 0; o < W; ++o) {
+          float acc_o = b0[o];
+          for (int k = 0; k < s.d0; ++k) acc_o = fmaf(W0[o * s.d0 + k], x[k], acc_o);
+          h[o] = simt_act(acc_o, s.act);
+        }
+      } else {
+        float f[kSimtMaxIn];
+        simt_features(x, s.d0, s.pe, f);
+#pragma unroll
+        for (int o = 0; o < W; ++o) {
+          float acc_o = b0[o];
+          for (int k = 0; k < s.din; ++k) acc_o = fmaf(W0[o * s.din + k], f[k], acc_o);
+          h[o] = simt_act(acc_o, s.act);
+        }
       }
     }
     for (int l = 1; l <= s.L; ++l) {
@@ -243,7 +274,7 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
           float acc_o = bl[o];
 #pragma unroll
           for (int k = 0; k < W; ++k) acc_o = fmaf(Wl[o * W + k], h[k], acc_o);
-          hn[o] = fmaxf(acc_o, 0.f);
+          hn[o] = simt_act(acc_o, s.act);
         }
 #pragma unroll
         for (int o = 0; o < W; ++o) h[o] = hn[o];
@@ -286,8 +317,9 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
 }
 
 bool simt_supported(const nb_desc& d) {
+  const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
   return (d.width == 16 || d.width == 32 || d.width == 64) && d.hidden_layers >= 1 &&
-         d.hidden_layers <= kMaxLayers;
+         d.hidden_layers <= kMaxLayers && r * (1 + d.pe_depth) <= kSimtMaxIn;
 }
 
 template <int W>
@@ -296,6 +328,9 @@ static cudaError_t launch_simt_w(const nb_model* m, int mode, const FwdArgs& a, 
   s.po = m->po;
   s.P = (int)m->P;
   s.d0 = m->d0;
+  s.din = m->din;
+  s.act = m->d.activation;
+  s.pe = m->d.pe_depth;
   s.L = m->d.hidden_layers;
   s.nh = m->d.n_heads;
   s.ha0 = m->d.head_after[0];
@@ -348,7 +383,7 @@ struct TrainScratch {
 
 static TrainScratch carve_simt(nb_model* m, int64_t n) {
   const int W = m->d.width, L = m->d.hidden_layers, nh = m->d.n_heads;
-  const int Wm = std::max(W, m->d0);
+  const int Wm = std::max(W, m->din);
   uint8_t* p = (uint8_t*)m->train_scratch;
   TrainScratch t;
   t.h = (float*)p; p += sizeof(float) * (size_t)(L + 1) * n * Wm;
@@ -360,7 +395,7 @@ static TrainScratch carve_simt(nb_model* m, int64_t n) {
 
 size_t train_simt_scratch_bytes(const nb_model* m, int64_t n) {
   const int W = m->d.width, L = m->d.hidden_layers, nh = m->d.n_heads;
-  const int Wm = std::max(W, m->d0);
+  const int Wm = std::max(W, m->din);
   return sizeof(float) * ((size_t)(L + 1) * n * Wm + (size_t)L * n * W + (size_t)n * (1 + nh) +
                           (size_t)kGradChunks * m->P) + 256;
 }
@@ -380,25 +415,32 @@ __global__ void __launch_bounds__(128) k_train_fwd_bwd_simt(const float* __restr
   extern __shared__ float sp[];
   for (int i = threadIdx.x; i < s.P; i += blockDim.x) sp[i] = theta[i];
   __syncthreads();
-  const int Wm = W > s.d0 ? W : s.d0;
+  const int Wm = W > s.din ? W : s.din;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool valid = i < n;
   float loss = 0.f;
   unsigned st[4] = {0, 0, 0, 0};
   if (valid) {
-    float hs[kMaxLayers + 1][W];  // h_0 (padded) .. h_L
+    float hs[kMaxLayers + 1][W];  // h_0 (layer-1 input, din <= W) .. h_L
+    float ds[kMaxLayers][W];      // activation derivative at z_l (ReLU mask, or cos z_l)
+    {
+      float x[8], f[kSimtMaxIn];
+      for (int j = 0; j < 8; ++j) x[j] = j < s.d0 ? q[i * s.d0 + j] : 0.f;
+      simt_features(x, s.d0, s.pe, f);
 #pragma unroll
-    for (int j = 0; j < W; ++j) hs[0][j] = j < s.d0 ? q[i * s.d0 + j] : 0.f;
+      for (int j = 0; j < W; ++j) hs[0][j] = j < s.din ? f[j] : 0.f;
+    }
     float e[2] = {0.f, 0.f};
     for (int l = 1; l <= s.L; ++l) {
-      const int in = l == 1 ? s.d0 : W;
+      const int in = l == 1 ? s.din : W;
       const float* Wl = sp + s.po.W[l - 1];
       const float* bl = sp + s.po.b[l - 1];
 #pragma unroll
       for (int o = 0; o < W; ++o) {
         float a = bl[o];
         for (int k = 0; k < in; ++k) a = fmaf(Wl[o * in + k], hs[l - 1][k], a);
-        hs[l][o] = fmaxf(a, 0.f);
+        hs[l][o] = simt_act(a, s.act);
+        ds[l - 1][o] = simt_dact(a, s.act);
       }
       for (int k = 0; k < s.nh; ++k)
         if ((k == 0 ? s.ha0 : s.ha1) == l) {
@@ -439,11 +481,11 @@ __global__ void __launch_bounds__(128) k_train_fwd_bwd_simt(const float* __restr
       float* drow = t.dlt + ((int64_t)(l - 1) * n + i) * W;
 #pragma unroll
       for (int j = 0; j < W; ++j) {
-        dh[j] = hs[l][j] > 0.f ? dh[j] : 0.f;
+        dh[j] *= ds[l - 1][j];
         drow[j] = dh[j];
       }
       float* hrow = t.h + ((int64_t)(l - 1) * n + i) * Wm;
-      const int in = l == 1 ? s.d0 : W;
+      const int in = l == 1 ? s.din : W;
       for (int k = 0; k < in; ++k) hrow[k] = hs[l - 1][k];
       if (l > 1) {
         const float* Wl = sp + s.po.W[l - 1];
@@ -556,6 +598,9 @@ cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int
   s.nh = m->d.n_heads;
   s.ha0 = m->d.head_after[0];
   s.ha1 = m->d.head_after[1];
+  s.din = m->din;
+  s.act = m->d.activation;
+  s.pe = m->d.pe_depth;
   TrainScratch t = carve_simt(m, n);
   const float invB = 1.0f / (float)n_global;
   const size_t smem = sizeof(float) * m->P;
@@ -579,7 +624,7 @@ cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int
   GradArgs g;
   g.po = m->po;
   g.P = (int)m->P;
-  g.d0 = m->d0;
+  g.d0 = m->din;  // layer-1 input features
   g.W = m->d.width;
   g.L = m->d.hidden_layers;
   g.nh = m->d.n_heads;
@@ -707,7 +752,7 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
   a.po = m->po;
   a.W = m->d.width;
   a.L = m->d.hidden_layers;
-  a.d0 = m->d0;
+  a.d0 = m->din;
   a.nh = m->d.n_heads;
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
   k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P,

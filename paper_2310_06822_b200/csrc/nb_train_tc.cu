@@ -460,8 +460,9 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
 // host side
 // ---------------------------------------------------------------------------
 bool train_tc_supported(const nb_desc& d) {
+  // sine / positional-encoding nets train on the fp32 path (DESIGN.md §8 NEXT)
   return d.precision == NB_BF16 && (d.width == 64 || d.width == 128 || d.width == 256) &&
-         d.hidden_layers >= 2;
+         d.hidden_layers >= 2 && d.activation == NB_RELU && d.pe_depth == 0;
 }
 
 struct TrainLayout {

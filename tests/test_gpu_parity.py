@@ -685,3 +685,77 @@ def test_exit_compaction_nonfinite_and_async_paths():
     clean = m.score(cuda(q), cuda(y))
     h = m.score_host(q.contiguous(), torch.from_numpy(y).contiguous())
     assert h == clean
+
+
+# ---------------------------------------------------------------- NEXT-1: sine + positional encoding
+def _sine_case(name, width, layers, pe, precision, n, seed=0, scale=0.9):
+    cfg = nbgen.CONFIGS[name]
+    desc = nb.Desc(cfg.kind, cfg.space_dim, width, layers, (), precision, activation="sine",
+                   pe_depth=pe)
+    a = oracle.make_arch(cfg.record_floats, width, layers, act="sine", pe=pe)
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, seed, n)
+    y = labels_oracle(cfg, q.numpy())
+    rng = np.random.default_rng(seed + 5)
+    th = rng.uniform(-1, 1, oracle.num_params(a)) * scale * np.sqrt(6.0 / (width + width))
+    return cfg, desc, a, q, y, th
+
+
+@pytest.mark.parametrize("pe", [0, 8])
+def test_fp32_sine_pe_forward_and_gradient(pe):
+    """fp32 path (P1 / P3 tolerances) with the paper's sine activation
+    and the NeRF encoding (Suppl. §3; 2D points, depth 8 -> 18 inputs)."""
+    cfg, desc, a, q, y, th = _sine_case("c1", 32, 2, pe, "fp32", 4096 + 77)
+    m = nb.Model(desc, DEV)
+    m.set_params(torch.from_numpy(th).float())
+    th32 = torch.from_numpy(th).float().double().numpy()
+    z = m.forward(cuda(q)).cpu().double().numpy()[:, 0]
+    zr = oracle.forward(a, th32, q.numpy())[:, 0]
+    assert np.all(np.abs(z - zr) <= 1e-5 * np.maximum(1.0, np.abs(zr)))
+    st = m.train_step(cuda(q), cuda(y), alpha=9.0, beta=0.7, lr=1e-3, stats=True)
+    g = m.get_grad().double().numpy()
+    loss, gr, sr = oracle.loss_grad(a, th32, q.numpy(), y, 9.0, 0.7)
+    assert abs(st["loss"] - loss) <= 1e-4 * abs(loss)
+    assert np.linalg.norm(g - gr) <= 1e-4 * np.linalg.norm(gr)
+
+
+@pytest.mark.parametrize("name,width,layers,pe,n", [("c2", 64, 3, 0, (1 << 15) + 77),
+                                                    ("c1", 128, 3, 8, (1 << 15) + 5),
+                                                    ("c2", 128, 2, 4, (1 << 14) + 3)])
+def test_bf16_sine_pe_forward_and_counts(name, width, layers, pe, n):
+    """bf16 tensor-core path with sine epilogues (range-reduced SFU sine) and
+    the in-kernel positional encoding (layer-1 K up to 64): sigmoid within
+    2e-2 of the fp64 definition, counts equal to the bf16-emulating oracle's
+    outside the threshold band, FN = 0 on the calibration set."""
+    cfg, desc, a, q, y, th = _sine_case(name, width, layers, pe, "bf16", n)
+    m = nb.Model(desc, DEV)
+    m.set_params(torch.from_numpy(th).float())
+    th32 = torch.from_numpy(th).float().double().numpy()
+    qd, yd = cuda(q), cuda(y)
+    z, p = m.forward(qd, prob=True)
+    zr = oracle.forward(a, th32, q.numpy())[:, 0]
+    assert np.max(np.abs(p.cpu().double().numpy() - 1 / (1 + np.exp(-zr)))) <= 2e-2
+    tau = m.calibrate(qd, yd).numpy()
+    c = m.score(qd, yd)
+    assert c["fn"] == 0
+    ze = oracle.forward(a, th32, q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    zg = z.cpu().double().numpy()
+    keep = ~band_mask(zg, tau, ze, te)
+    assert keep.mean() > 0.95
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    for k in ("tp", "fp", "fn", "tn"):
+        assert cg[k] == co[k], (k, cg, co)
+
+
+def test_sine_pe_unsupported_paths_fail_loudly():
+    """bf16 training of sine / PE nets and nb_encode with PE are not built:
+    they return NB_E_UNSUPPORTED instead of computing something else."""
+    cfg, desc, a, q, y, th = _sine_case("c2", 64, 3, 2, "bf16", 1024)
+    m = nb.Model(desc, DEV)
+    m.set_params(torch.from_numpy(th).float())
+    with pytest.raises(nb.NBError) as ei:
+        m.train_step(cuda(q), cuda(y), alpha=2.0)
+    assert "UNSUPPORTED" in str(ei.value)
+    with pytest.raises(nb.NBError):
+        m.encode(cuda(q))
