@@ -90,7 +90,9 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   pl->pairs = (d.precision == NB_BF16 && W > 128) ? 2u : 1u;
   const uint32_t rows = W / pl->pairs;
   const int din = input_features(d);
-  const uint32_t K0 = enc_k(din);
+  const bool pe_split = d.pe_depth > 0 && d.precision == NB_BF16;
+  const uint32_t K0 = pe_split ? 64u : (uint32_t)enc_k(din);
+  pl->pe_lo = pe_split ? 32u : 0u;
   for (int l = 0; l < d.hidden_layers; ++l) {
     const uint32_t K = l == 0 ? K0 : W;
     pl->off_w[l] = off;
@@ -109,7 +111,7 @@ static void pack_layout(const nb_desc& d, PackLayout* pl) {
   pl->core_bytes = off;
   const bool shared = pl->pairs == 2 && d.precision == NB_BF16 && 3 * (d.hidden_layers - 1) <= kEncK;
   const bool fold = (pl->pairs == 1 && d.precision == NB_BF16) || shared;
-  pl->bias_l0 = (fold && 2 * din + 3 <= (int)K0) ? 1u : 0u;
+  pl->bias_l0 = (fold && (pe_split ? din + 3 <= 32 : 2 * din + 3 <= (int)K0)) ? 1u : 0u;
   pl->bb_shared = shared ? 1u : 0u;
   for (int l = 0; l < kMaxLayers; ++l) pl->off_bb[l] = 0;
   if (shared) {

@@ -10,8 +10,9 @@ bool tc_supported(const nb_desc& d) {
   if (d.hidden_layers < 1 || d.hidden_layers > kMaxLayers) return false;
   // layer-1 operand (hi, lo and bias columns) fits the slot's A region
   const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
-  const int k0 = enc_k(r * (1 + d.pe_depth));
-  return k0 <= kTcMaxEncK && k0 <= d.width;
+  if (d.pe_depth > 0)  // PE operand layout: d_in + 3 <= 32, K = 64 (PackLayout::pe_lo)
+    return d.width >= 64 && r * (1 + d.pe_depth) + 3 <= 32;
+  return enc_k(r) <= d.width;
 }
 
 // NB_TRACE builds: device buffer set by nb_debug_set_trace (tools/trace_fwd.py).

@@ -97,41 +97,51 @@ __device__ __forceinline__ void encode_cols(const float* x, int d0_rt, uint32_t 
   for (int c = 0; c < 8; ++c) col[c] = e[2 * c] | (e[2 * c + 1] << 16);
 }
 
-// a1 encode with positional encoding (generic kernels, R42): the
-// d_in = d0 (1 + pe) features [x, sin(2^k pi x), cos(2^k pi x) per frequency]
-// of one record, each split into a bf16 (hi, lo) pair, then three 1.0 bias
-// columns; K0 / 2 packed 32-bit columns (K0 = enc_k(d_in) <= 64).
-__device__ __forceinline__ void encode_cols_pe(const float* x, int d0, int pe, int k0, uint32_t (&col)[32]) {
-  float f[kTcMaxEncK / 2];
-  const int din = d0 * (1 + pe);
-  for (int j = 0; j < d0; ++j) f[j] = x[j];
-  for (int k = 0; k < pe / 2; ++k)
-    for (int j = 0; j < d0; ++j) {
-      float sv, cv;
-      sincospif(ldexpf(x[j], k), &sv, &cv);
-      f[d0 + 2 * k * d0 + j] = sv;
-      f[d0 + (2 * k + 1) * d0 + j] = cv;
+// a1 encode with positional encoding (EXT kernels, R42): the
+// d_in = D0 (1 + pe) features [x, sin(2^k pi x), cos(2^k pi x) per frequency]
+// of one record, each split into a bf16 (hi, lo) pair, in the PE operand
+// layout (PackLayout::pe_lo): hi at [0, d_in), the bias ones at
+// [d_in, d_in + 3), lo at [32, 32 + d_in); K = 64, 32 packed columns.  D0 is
+// compile-time so every feature index is a register.
+template <int D0>
+__device__ __forceinline__ void encode_cols_pe(const float* x, int pe, uint32_t (&col)[32]) {
+  constexpr int kMaxF = 29;  // d_in + 3 <= 32
+  const int din = D0 * (1 + pe);
+  float f[kMaxF];
+#pragma unroll
+  for (int j = 0; j < kMaxF; ++j) f[j] = j < D0 ? x[j] : 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (2 * k < pe) {
+#pragma unroll
+      for (int j = 0; j < D0; ++j) {
+        float sv, cv;
+        sincospif(ldexpf(x[j], k), &sv, &cv);
+        if (D0 + 2 * k * D0 + j < kMaxF) f[D0 + 2 * k * D0 + j] = sv;
+        if (D0 + (2 * k + 1) * D0 + j < kMaxF) f[D0 + (2 * k + 1) * D0 + j] = cv;
+      }
     }
-  auto elem = [&](int k) -> uint32_t {
-    if (k < din) return __bfloat16_as_ushort(__float2bfloat16_rn(f[k]));
-    if (k < 2 * din) {
-      const float v = f[k - din];
-      return __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(__float2bfloat16_rn(v))));
+  }
+  uint32_t e[64];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t hi = k < kMaxF ? __bfloat16_as_ushort(__float2bfloat16_rn(f[k < kMaxF ? k : 0])) : 0u;
+    e[k] = k < din ? hi : (k < din + 3 ? 0x3F80u : 0u);
+    uint32_t lo = 0u;
+    if (k < kMaxF) {
+      const float v = f[k];
+      lo = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(__float2bfloat16_rn(v))));
     }
-    return k < 2 * din + 3 ? 0x3F80u : 0u;
-  };
-  for (int c = 0; c < 32; ++c) col[c] = 2 * c < k0 ? (elem(2 * c) | (elem(2 * c + 1) << 16)) : 0u;
+    e[32 + k] = k < din ? lo : 0u;
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) col[c] = e[2 * c] | (e[2 * c + 1] << 16);
 }
 
-// sine hidden activation (R41): 2 pi range reduction in fp32
-// (two-constant Cody-Waite), then the SFU sine on [-pi, pi]: |error| ~ 1e-6,
-// far below the bf16 rounding of the result
-__device__ __forceinline__ float sin_act(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  float r = fmaf(-k, 6.28318548202514648f, x);
-  r = fmaf(-k, -1.74845553e-7f, r);
-  return __sinf(r);
-}
+// sine hidden activation (R41): the SFU sine (sin.approx:
+// x / 2 pi, then MUFU.SIN); |error| <= ~2^-21 + |x| 2^-22, i.e. < 3e-5 for
+// |x| < 100 — far below the bf16 rounding (2^-9 relative) of the result
+__device__ __forceinline__ float sin_act(float x) { return __sinf(x); }
 
 __device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{.reg .b64 ra, rb, rd;\n\t"
@@ -442,10 +452,11 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         for (int j = 0; j < 8; ++j) x[j] = (v && j < d0) ? __ldg(p.a.q + r * d0 + j) : 0.f;
         ycur = (MODE != kForward && v) ? (int)__ldg(p.a.y + r) : 0;
       }
-      if (EXT && p.pe > 0) {
+      if (EXT && D0C > 0) {  // positional encoding (D0C = record floats)
         uint32_t c[32];
-        encode_cols_pe(x, d0, p.pe, p.k0, c);
-        for (int g = 0; g < p.k0 / 16; ++g)
+        encode_cols_pe<D0C>(x, p.pe, c);
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
           tmem_st8(trow + a_col(s) + (uint32_t)(8 * g), *reinterpret_cast<const uint32_t(*)[8]>(c + 8 * g));
       } else {
         uint32_t c[8];
@@ -692,14 +703,18 @@ inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   return cudaGetLastError();
 }
 
-// Generic sine / PE kernels (bias folded; forward, calibrate, score).
-template <int W>
-inline cudaError_t launch_tc_ext(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
-  if (mode == kForward) return launch_tc_wm<W, 0, 0, 0, kForward, 0, true, true>(m, a, st);
-  if (mode == kCalibrate) return launch_tc_wm<W, 0, 0, 0, kCalibrate, 0, true, true>(m, a, st);
-  if (mode == kScore) return launch_tc_wm<W, 0, 0, 0, kScore, 0, true, true>(m, a, st);
+// Generic sine / PE kernels (bias folded; forward, calibrate, score).  D0 > 0:
+// positional encoding of D0-float records; D0 = 0: no encoding (sine only).
+template <int W, int D0>
+inline cudaError_t launch_tc_ext_d(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (mode == kForward) return launch_tc_wm<W, 0, 0, 0, kForward, D0, true, true>(m, a, st);
+  if (mode == kCalibrate) return launch_tc_wm<W, 0, 0, 0, kCalibrate, D0, true, true>(m, a, st);
+  if (mode == kScore) return launch_tc_wm<W, 0, 0, 0, kScore, D0, true, true>(m, a, st);
   return cudaErrorInvalidValue;
 }
+cudaError_t launch_tc_ext32(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_tc_ext64(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
+cudaError_t launch_tc_ext128(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);
 
 template <int W, int LC, int H0C, int H1C, int D0C, bool BF>
 inline cudaError_t launch_tc_modes(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {

@@ -5,7 +5,7 @@
 namespace nb {
 
 cudaError_t launch_tc_gen64(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st, bool fold) {
-  if (m->d.activation != NB_RELU || m->d.pe_depth > 0) return launch_tc_ext<64>(m, mode, a, st);
+  if (m->d.activation != NB_RELU || m->d.pe_depth > 0) return launch_tc_ext64(m, mode, a, st);
   return fold ? launch_tc_modes<64, 0, 0, 0, 0, true>(m, mode, a, st)
               : launch_tc_modes<64, 0, 0, 0, 0, false>(m, mode, a, st);
 }

@@ -48,6 +48,11 @@ struct PackLayout {
   // bias_l0 != 0 (the in-kernel encoder puts ones there).
   uint32_t off_bb[kMaxLayers];
   uint32_t bias_l0;
+  uint32_t pe_lo;
+  // positional-encoding nets (bf16): layer 1 is K = 64 with hi halves in
+  // columns [0, d_in), the bias ones at [d_in, d_in + 3) and lo halves at
+  // [pe_lo, pe_lo + d_in), pe_lo = 32 (compile-time operand indices in the
+  // encoder); 0 = the default [hi | lo | ones] order
   // CTA-pair images (pairs == 2): ONE shared [rows][16] bias block at
   // off_bb[0] holds the split of every hidden layer l >= 1 in columns
   // 3 (l - 1) .. 3 (l - 1) + 2 (a per-layer ones block in TMEM selects them)

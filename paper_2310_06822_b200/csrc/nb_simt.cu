@@ -93,7 +93,13 @@ __global__ void k_pack_bf16(PackArgs a) {
     for (int64_t e = tid; e < (int64_t)W * K; e += stride) {
       int n = (int)(e / K), k = (int)(e % K);
       float v;
-      if (l == 0) {
+      if (l == 0 && a.pl.pe_lo) {  // PE layout: [hi | ones | .. | lo at pe_lo]
+        const int lo = (int)a.pl.pe_lo;
+        int src = k < a.d0 ? k : ((k >= lo && k < lo + a.d0) ? k - lo : -1);
+        v = src >= 0 ? a.theta[a.po.W[0] + (int64_t)n * a.d0 + src] : 0.f;
+        const int j = k - a.d0;
+        if (a.pl.bias_l0 && j >= 0 && j < 3) v = bias_piece(a.theta[a.po.b[0] + n], j);
+      } else if (l == 0) {
         int src = k < a.d0 ? k : (k < 2 * a.d0 ? k - a.d0 : -1);
         v = src >= 0 ? a.theta[a.po.W[0] + (int64_t)n * a.d0 + src] : 0.f;
         const int j = k - 2 * a.d0;  // bias split columns (the encoder's ones)
