@@ -458,6 +458,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
 #pragma unroll
         for (int g = 0; g < 4; ++g)
           tmem_st8(trow + a_col(s) + (uint32_t)(8 * g), *reinterpret_cast<const uint32_t(*)[8]>(c + 8 * g));
+        if (MODE == kTrain) {  // layer-1 input image (F = 64) for the dW GEMM
+          uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(64);
+#pragma unroll
+          for (int fg = 0; fg < 8; ++fg)
+            *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+        }
       } else {
         uint32_t c[8];
         encode_cols<D0C, BF>(x, d0, c);
@@ -548,6 +555,16 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
             for (int i = 0; i < 4; ++i)
               *reinterpret_cast<uint4*>(base + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
                   make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            if (EXT && p.act == NB_SINE) {  // sigma'(z) = cos z for the backward chain (R41)
+              uint32_t ck[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) ck[j] = pack_bf16x2(__cosf(t[2 * j]), __cosf(t[2 * j + 1]));
+              uint8_t* cb = p.a.tr.c_img[l] + tile * img_tile_bytes(W);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<uint4*>(cb + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                    make_uint4(ck[4 * i], ck[4 * i + 1], ck[4 * i + 2], ck[4 * i + 3]);
+            }
           }
         }
         if (l == h0 || l == h1 || last) {
@@ -710,6 +727,7 @@ inline cudaError_t launch_tc_ext_d(const nb_model* m, int mode, const FwdArgs& a
   if (mode == kForward) return launch_tc_wm<W, 0, 0, 0, kForward, D0, true, true>(m, a, st);
   if (mode == kCalibrate) return launch_tc_wm<W, 0, 0, 0, kCalibrate, D0, true, true>(m, a, st);
   if (mode == kScore) return launch_tc_wm<W, 0, 0, 0, kScore, D0, true, true>(m, a, st);
+  if (mode == kTrain && W >= 64) return launch_tc_wm<W, 0, 0, 0, kTrain, D0, true, true>(m, a, st);
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tc_ext32(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st);

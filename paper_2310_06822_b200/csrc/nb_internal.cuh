@@ -145,7 +145,8 @@ enum Mode { kForward = 0, kCalibrate = 1, kScore = 2, kTrain = 3 };
 // tile t at t * F * 256 bytes; consumed directly by the dW GEMM (bulk copy).
 struct TrainArgs {
   uint8_t* x_img;                // encoded layer-1 input, F = 16
-  uint8_t* h_img[kMaxLayers];    // h_l (post-ReLU, bf16), F = w, l = 1..L
+  uint8_t* h_img[kMaxLayers];    // h_l (post-activation, bf16), F = w, l = 1..L
+  uint8_t* c_img[kMaxLayers];    // sine nets: cos(z_l) (bf16), F = w — the activation derivative
   uint8_t* hd_img;               // [dL/dz, dL/de_1, dL/de_2, 0..] bf16, F = 8
   float* g32;                    // fp32 [n][3]: dL/dz, dL/de_1, dL/de_2
   float alpha, beta, inv_b;      // Eq. (1) weights, 1 / n_global

@@ -703,7 +703,8 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
         const int n = (int)((i - ow) / in), k = (int)((i - ow) % in);
         uint8_t* img = a.out + (size_t)(n / rows) * a.pl.bytes + a.pl.off_w[l];
         store_bf16(img, (int)a.pl.k_of[l], n % rows, k, t);
-        if (l == 0) store_bf16(img, (int)a.pl.k_of[0], n % rows, a.d0 + k, t);  // lo copy
+        if (l == 0)  // lo copy (after hi, or at pe_lo for PE nets)
+          store_bf16(img, (int)a.pl.k_of[0], n % rows, (a.pl.pe_lo ? (int)a.pl.pe_lo : a.d0) + k, t);
         if (l > 0 && a.out_bwd)  // transposed pair image: row = input feature k, column = n
           store_bf16(a.out_bwd + (size_t)(k / rows) * a.bl.bytes + a.bl.off_wt[l], W, k % rows, n, t);
         done = true;
@@ -713,7 +714,8 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
         uint8_t* imgb = a.out + (size_t)(n / rows) * a.pl.bytes;  // the image holding row n
         if (l == 0 && a.pl.bias_l0) {
           for (int j = 0; j < 3; ++j)
-            store_bf16(imgb + a.pl.off_w[0], kEncK, n % rows, 2 * a.d0 + j, bias_piece(t, j));
+            store_bf16(imgb + a.pl.off_w[0], (int)a.pl.k_of[0], n % rows,
+                       (a.pl.pe_lo ? 1 : 2) * a.d0 + j, bias_piece(t, j));
         } else if (l > 0 && a.pl.bb_shared) {
           for (int j = 0; j < 3; ++j)
             store_bf16(imgb + a.pl.off_bb[0], kEncK, n % rows, 3 * (l - 1) + j, bias_piece(t, j));

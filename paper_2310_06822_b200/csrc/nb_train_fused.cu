@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fused(const FusedParams p) {
 bool train_fused_supported(const nb_model* m) {
   const nb_desc& d = m->d;
   return d.precision == NB_BF16 && d.width == kFusedW && d.n_heads == 0 && d.hidden_layers >= 2 &&
+         d.activation == NB_RELU && d.pe_depth == 0 &&
          d.hidden_layers <= 4 && m->pl.pairs == 1 && m->pl.bias_l0 && 2 * m->d0 + 3 <= kEncK;
 }
 

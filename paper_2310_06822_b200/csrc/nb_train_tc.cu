@@ -37,6 +37,8 @@ struct BwdParams {
   const uint8_t* h_img[kMaxLayers];  // h_1..h_L images (F = W)
   uint8_t* d_img[kMaxLayers];        // delta_1..delta_L images (F = W)
   const float* g32;                  // [n][3]
+  const uint8_t* c_img[kMaxLayers];  // sine nets: cos(z_l) images; delta = g * cos (R41)
+  int sine;
 };
 
 __device__ __forceinline__ uint32_t img_off(int r, int fg) {
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   // step ahead into registers.
   constexpr int HW = W / 8;  // uint4 per h row
   auto load_h = [&](uint4 (&h)[HW], int l1, int64_t t) {  // h_{l1} row of tile t (l1 1-based)
-    const uint8_t* hrow = p.h_img[l1 - 1] + t * img_tile_bytes(W);
+    const uint8_t* hrow = (p.sine ? p.c_img[l1 - 1] : p.h_img[l1 - 1]) + t * img_tile_bytes(W);
 #pragma unroll
     for (int q = 0; q < HW; ++q) h[q] = *reinterpret_cast<const uint4*>(hrow + img_off(rit, q));
   };
@@ -149,8 +151,14 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int i = 8 * q + 2 * e;
-            const float m0 = (hw[e] & 0x7FFFu) ? g[i] : 0.f;           // h > 0 (h >= 0 by ReLU)
-            const float m1 = (hw[e] & 0x7FFF0000u) ? g[i + 1] : 0.f;
+            float m0, m1;
+            if (p.sine) {  // g * cos(z_l)
+              m0 = g[i] * __uint_as_float(hw[e] << 16);
+              m1 = g[i + 1] * __uint_as_float(hw[e] & 0xFFFF0000u);
+            } else {
+              m0 = (hw[e] & 0x7FFFu) ? g[i] : 0.f;           // h > 0 (h >= 0 by ReLU)
+              m1 = (hw[e] & 0x7FFF0000u) ? g[i + 1] : 0.f;
+            }
             pk[4 * q + e] = pack_bf16x2(m0, m1);
           }
         }
@@ -212,6 +220,7 @@ struct DwJob {
   int kind;      // 0: W[m][k] <- D[m][k], b[m] <- D[m][fb]
                  // 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
                  // 2: head row `row`: v[j] <- D[row][j], c <- D[row][fb]
+                 // 3: layer 1 of a PE net (PackLayout::pe_lo): W[m][j] <- D[m][j] + D[m][32 + j], b[m] <- D[m][fb]
   int rows, row, d0, in;
   float* w_out;
   float* b_out;
@@ -406,7 +415,7 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
     k = (int)(e / rows);                          // output column (k == in: bias)
     m = r.kind == 2 ? r.row : (int)(e % rows);    // row of D
     const int c0 = k == r.in ? r.fb : k;
-    const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : -1;
+    const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : ((k != r.in && r.kind == 3) ? 32 + k : -1);
     const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
     const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
     const int per = (js.cpj + kRedSlices - 1) / kRedSlices;
@@ -460,13 +469,14 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
 // host side
 // ---------------------------------------------------------------------------
 bool train_tc_supported(const nb_desc& d) {
-  // sine / positional-encoding nets train on the fp32 path (DESIGN.md §8 NEXT)
-  return d.precision == NB_BF16 && (d.width == 64 || d.width == 128 || d.width == 256) &&
-         d.hidden_layers >= 2 && d.activation == NB_RELU && d.pe_depth == 0;
+  // sine / positional-encoding nets: w = 64, 128 (the EXT forward kernels, R41, R42)
+  const bool plain = d.activation == NB_RELU && d.pe_depth == 0;
+  return d.precision == NB_BF16 && (d.width == 64 || d.width == 128 || (d.width == 256 && plain)) &&
+         d.hidden_layers >= 2;
 }
 
 struct TrainLayout {
-  size_t x_img, h_img[kMaxLayers], d_img[kMaxLayers], hd_img, g32, partial, total;
+  size_t x_img, h_img[kMaxLayers], c_img[kMaxLayers], d_img[kMaxLayers], hd_img, g32, partial, total;
 };
 
 static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
@@ -479,8 +489,10 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
     off += (bytes + 255) & ~(size_t)255;
     return o;
   };
-  t.x_img = take(T * img_tile_bytes(16));
+  t.x_img = take(T * img_tile_bytes((int)m->pl.k_of[0]));
   for (int l = 0; l < L; ++l) t.h_img[l] = take(T * img_tile_bytes(W));
+  const bool sine = m->d.activation == NB_SINE;
+  for (int l = 0; l < L; ++l) t.c_img[l] = sine ? take(T * img_tile_bytes(W)) : 0;
   for (int l = 0; l < L; ++l) t.d_img[l] = take(T * img_tile_bytes(W));
   // the dW GEMM reads 128 features of A per tile: pad the last tile's images
   take(img_tile_bytes(128));
@@ -531,7 +543,7 @@ static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
 // last.  (L2-sized micro-batches of ~64 MB were measured slower: the kernels
 // are latency-bound below ~2^16 rows, e.g. c5 2^18 rows 0.74 -> 2.9 ms.)
 static int64_t train_chunk_rows(const nb_model* m, int64_t n) {
-  const int64_t per_row = 2 * (16 + 2 * (int64_t)m->d.hidden_layers * m->d.width + 8) + 12;
+  const int64_t per_row = 2 * ((int64_t)m->pl.k_of[0] + 3 * (int64_t)m->d.hidden_layers * m->d.width + 8) + 12;
   int64_t c = ((int64_t)2 << 30) / per_row;
   if (const char* ev = getenv("NB_TRAIN_CHUNK")) c = atoll(ev);  // test / measurement override
   c = std::max<int64_t>(256, c / 256 * 256);
@@ -563,7 +575,9 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
   a.keys = m->d_keys;
   a.flags = m->d_flags;
   a.tr.x_img = base + tl.x_img;
+  const bool sine = m->d.activation == NB_SINE;
   for (int l = 0; l < L; ++l) a.tr.h_img[l] = base + tl.h_img[l];
+  for (int l = 0; l < L; ++l) a.tr.c_img[l] = sine ? base + tl.c_img[l] : nullptr;
   a.tr.hd_img = base + tl.hd_img;
   a.tr.g32 = (float*)(base + tl.g32);
   a.tr.alpha = alpha;
@@ -588,7 +602,9 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
   for (int l = 0; l < L; ++l) {
     bp.h_img[l] = base + tl.h_img[l];
     bp.d_img[l] = base + tl.d_img[l];
+    bp.c_img[l] = sine ? base + tl.c_img[l] : nullptr;
   }
+  bp.sine = sine ? 1 : 0;
   bp.g32 = (float*)(base + tl.g32);
   if (pairs)
     e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st);
@@ -633,7 +649,9 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     }
   };
   for (int l = 0; l < L; ++l) {
-    if (l == 0)
+    if (l == 0 && m->pl.pe_lo)  // PE operand: hi [0, d_in), lo [32, 32 + d_in), K = 64
+      add(base + tl.d_img[0], W, base + tl.x_img, 64, 3, W, 0, m->din, g + m->po.W[0], g + m->po.b[0]);
+    else if (l == 0)
       add(base + tl.d_img[0], W, base + tl.x_img, 16, 1, W, 0, d0, g + m->po.W[0], g + m->po.b[0]);
     else
       add(base + tl.d_img[l], W, base + tl.h_img[l - 1], W, 0, W, 0, W, g + m->po.W[l], g + m->po.b[l]);

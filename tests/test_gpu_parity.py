@@ -749,13 +749,54 @@ def test_bf16_sine_pe_forward_and_counts(name, width, layers, pe, n):
 
 
 def test_sine_pe_unsupported_paths_fail_loudly():
-    """bf16 training of sine / PE nets and nb_encode with PE are not built:
-    they return NB_E_UNSUPPORTED instead of computing something else."""
+    """nb_encode with PE (the kernels encode in place) and sine / PE nets on
+    CTA pairs (w = 256) are not built: NB_E_UNSUPPORTED, never a silent
+    fallback."""
     cfg, desc, a, q, y, th = _sine_case("c2", 64, 3, 2, "bf16", 1024)
     m = nb.Model(desc, DEV)
     m.set_params(torch.from_numpy(th).float())
     with pytest.raises(nb.NBError) as ei:
-        m.train_step(cuda(q), cuda(y), alpha=2.0)
+        m.encode(cuda(q))
     assert "UNSUPPORTED" in str(ei.value)
     with pytest.raises(nb.NBError):
-        m.encode(cuda(q))
+        nb.Model(nb.Desc("point", 3, 256, 3, (), "bf16", activation="sine"), DEV)
+
+
+def _tensor_slices(din, width, layers):
+    out, p, d_in = [], 0, din
+    for l in range(layers):
+        out.append((f"W{l + 1}", slice(p, p + d_in * width))); p += d_in * width
+        out.append((f"b{l + 1}", slice(p, p + width))); p += width
+        d_in = width
+    out.append(("w_out", slice(p, p + width))); p += width
+    out.append(("b_out", slice(p, p + 1)))
+    return out
+
+
+@pytest.mark.parametrize("name,width,layers,pe,n", [("c2", 64, 3, 0, (1 << 13) + 77),
+                                                    ("c2", 128, 3, 0, (1 << 12) + 5),
+                                                    ("c1", 128, 3, 8, (1 << 12) + 33),
+                                                    ("c2", 64, 2, 4, (1 << 12) + 9)])
+def test_bf16_sine_pe_train_step_gradient_parity(name, width, layers, pe, n):
+    """NEXT-1 training on tensor cores: the forward keeps cos(z_l) images for
+    the backward chain (delta = g cos z, R41) and the PE layer-1 image (K =
+    64); per-tensor gradient within 2e-2 of the oracle's bf16-precision
+    gradient, then the fused Adam + re-pack leaves exactly the image a full
+    pack builds (logits bit-identical)."""
+    cfg, desc, a, q, y, th = _sine_case(name, width, layers, pe, "bf16", n, seed=3)
+    m = nb.Model(desc, DEV)
+    m.set_params(torch.from_numpy(th).float())
+    th32 = torch.from_numpy(th).float().double().numpy()
+    alpha = 20.0
+    st = m.train_step(cuda(q), cuda(y), alpha=alpha, beta=1.0, lr=1e-3, stats=True)
+    g = m.get_grad().double().numpy()
+    le, ge_, _ = oracle.loss_grad(a, th32, q.numpy(), y, alpha, 1.0, mode=oracle.BF16_EMU)
+    assert abs(st["loss"] - le) <= 1e-3 * abs(le)
+    rel = {nm: np.linalg.norm(g[sl] - ge_[sl]) / np.linalg.norm(ge_[sl])
+           for nm, sl in _tensor_slices(cfg.record_floats * (1 + pe), width, layers)
+           if np.linalg.norm(ge_[sl]) > 0}
+    assert max(rel.values()) <= 2e-2, rel
+    m2 = nb.Model(desc, DEV)
+    m2.set_params(m.get_params())
+    qq = cuda(q[:1000])
+    assert torch.equal(m.forward(qq), m2.forward(qq))
