@@ -182,6 +182,16 @@ nb_status nb_forward(const nb_model* m, const float* q, int64_t n, float* logits
 nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n, float* tau_out,
                        void* stream);
 
+/* Inverted ("certainly hit") bounding ("conservatively bounds
+ * which spatial locations certainly are hit ... by flipping the asymmetry
+ * weights"; train with the FP weight ramped instead of the FN weight):
+ * tau = the next float above the maximum logit over labelled NEGATIVES, so
+ * the predictor z >= tau has FP = 0 on this set (R43).  Models
+ * without exit heads (NB_E_UNSUPPORTED otherwise); no negatives -> tau = +inf
+ * and the warning-class NB_E_NO_POSITIVES.  nb_score then counts with it.   */
+nb_status nb_calibrate_inverted(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                                float* tau_out, void* stream);
+
 /* a1-a5: fused forward + classify + count with the model's thresholds:
  * yhat = [e_1 >= tau_1] and [e_2 >= tau_2] and [z >= tau]; counts to *out (host).
  * Records with a non-finite logit are counted in out->nonfinite (a NaN never
@@ -252,8 +262,9 @@ nb_status nb_schedule_after_step(nb_schedule* s, uint64_t batch_fn);
 nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uint8_t* host,
                          int32_t device, nb_grid** out);
 void      nb_grid_destroy(nb_grid* g);
-/* y[i] = g(record i) exactly: point lookup, fp64 DDA for rays, SAT for boxes
- * (R15-R17; g = any f over the region).                    */
+/* y[i] = g(record i) exactly: point lookup, fp64 DDA for rays, SAT for boxes,
+ * fp64 voxel-corner cut test for planes (R15-R17, R19; g = any f
+ * over the region).  Rays, planes and boxes: 3D grids only.          */
 nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
                    void* stream);
 

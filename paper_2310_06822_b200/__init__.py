@@ -114,6 +114,7 @@ SIGNATURES = {
     "nb_forward": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
     "nb_calibrate": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_calibrate_inverted": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score_host": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score_async": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
@@ -323,6 +324,14 @@ class Model:
         ok = (NB_OK, NB_E_NO_POSITIVES) if allow_no_positives else (NB_OK,)
         _check(lib().nb_calibrate(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
                                   n, tau.data_ptr(), _stream(self.device)), "nb_calibrate", ok)
+        return tau
+
+    def calibrate_inverted(self, q: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        """Certainly-hit threshold (R43): FP = 0 on (q, y)."""
+        n = q.shape[0]
+        tau = torch.empty(self.nl, dtype=torch.float32)
+        _check(lib().nb_calibrate_inverted(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"),
+                                           n, tau.data_ptr(), _stream(self.device)), "nb_calibrate_inverted")
         return tau
 
     def score(self, q: torch.Tensor, y: torch.Tensor, allow_nonfinite: bool = False) -> dict:

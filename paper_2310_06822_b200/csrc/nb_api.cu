@@ -506,14 +506,18 @@ nb_status nb_forward(const nb_model* m, const float* q, int64_t n, float* logits
   return NB_OK;
 }
 
-nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n, float* tau_out,
-                       void* stream) {
+static nb_status calibrate_impl(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                                float* tau_out, void* stream, int invert) {
   if (!m || !tau_out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  if (invert && m->d.n_heads > 0)
+    return set_error("inverted calibration: models without exit heads"), NB_E_UNSUPPORTED;
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = 1 + m->d.n_heads;
   NB_CUDA(cudaMemsetAsync(m->d_keys, 0xFF, sizeof(unsigned int) * 4, s));
-  if (n > 0) NB_CUDA(launch_forward_any(m, kCalibrate, base_args(m, q, y, n), s));
+  FwdArgs a = base_args(m, q, y, n);
+  a.invert = invert;
+  if (n > 0) NB_CUDA(launch_forward_any(m, kCalibrate, a, s));
   if (m->comm && comm_allreduce_u32_min(m, m->d_keys, nl, s))
     return NB_E_NCCL;
   unsigned int* hk = (unsigned int*)m->h_pinned;
@@ -524,6 +528,8 @@ nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n,
     if (hk[k] == 0xFFFFFFFFu) {
       m->tau[k] = INFINITY;
       none = true;
+    } else if (invert) {  // the key holds min(-z) over negatives: tau = next float above max z
+      m->tau[k] = nextafterf(-key2f(hk[k]), INFINITY);
     } else {
       m->tau[k] = key2f(hk[k]);
     }
@@ -533,10 +539,20 @@ nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n,
   nb_status st = take_flags(m, s, NB_OK);
   if (st != NB_OK) return st;
   if (none) {
-    set_error("calibration set has no positives");
+    set_error(invert ? "calibration set has no negatives" : "calibration set has no positives");
     return NB_E_NO_POSITIVES;
   }
   return NB_OK;
+}
+
+nb_status nb_calibrate(nb_model* m, const float* q, const uint8_t* y, int64_t n, float* tau_out,
+                       void* stream) {
+  return calibrate_impl(m, q, y, n, tau_out, stream, 0);
+}
+
+nb_status nb_calibrate_inverted(nb_model* m, const float* q, const uint8_t* y, int64_t n,
+                                float* tau_out, void* stream) {
+  return calibrate_impl(m, q, y, n, tau_out, stream, 1);
 }
 
 // Score launches alternate between two counter sets / tickets: each launch's
@@ -817,6 +833,7 @@ nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uin
   if (e == cudaSuccess && space_dim == 3) {
     e = cudaMalloc((void**)&gr->sat, sizeof(int32_t) * (size_t)(R + 1) * (R + 1) * (R + 1));
     if (e == cudaSuccess) e = launch_sat_build(gr, 0);
+    if (e == cudaSuccess) e = launch_blk_build(gr, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   if (e != cudaSuccess) {
@@ -832,6 +849,7 @@ void nb_grid_destroy(nb_grid* g) {
   DeviceGuard dg(g->device);
   cudaFree(g->occ);
   cudaFree(g->sat);
+  cudaFree(g->blk);
   delete g;
 }
 
@@ -840,8 +858,8 @@ nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, ui
   if (!g || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
   if (kind == NB_POINT) {
     // ok for any dim
-  } else if (g->space_dim != 3 || (kind != NB_RAY && kind != NB_BOX)) {
-    set_error("GPU labeller supports points (2D/3D/4D), 3D rays and 3D boxes");
+  } else if (g->space_dim != 3 || (kind != NB_RAY && kind != NB_BOX && kind != NB_PLANE)) {
+    set_error("GPU labeller supports points (2D/3D/4D), 3D rays, planes and boxes");
     return NB_E_UNSUPPORTED;
   }
   if (n == 0) return NB_OK;

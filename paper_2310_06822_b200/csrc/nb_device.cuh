@@ -32,10 +32,10 @@ struct WarpAcc {
 template <int MODE>
 __device__ __forceinline__ void classify_row(WarpAcc& acc, bool valid, int y, float z,
                                              const float* e, int nh, const float* tau,
-                                             unsigned int* flags) {
+                                             unsigned int* flags, int invert = 0) {
   if (MODE == kCalibrate) {
-    if (valid && y == 1) {
-      acc.key[0] = min(acc.key[0], dkey(z));
+    if (valid && (invert ? y == 0 : y == 1)) {
+      acc.key[0] = min(acc.key[0], dkey(invert ? -z : z));
       if (nh > 0) acc.key[1] = min(acc.key[1], dkey(e[0]));
       if (nh > 1) acc.key[2] = min(acc.key[2], dkey(e[1]));
     }

@@ -165,11 +165,12 @@ __device__ __forceinline__ void fma2(float& c0, float& c1, float a0, float a1, f
 template <int MODE, int NHC>
 __device__ __forceinline__ void classify_row_smem(uint32_t* cnt, uint32_t (&key)[3], bool valid,
                                                   int y, float z, const float* e, int nh_rt,
-                                                  const float* tau, unsigned int* flags) {
+                                                  const float* tau, unsigned int* flags,
+                                                  int invert = 0) {
   const int nh = NHC >= 0 ? NHC : nh_rt;
   if (MODE == kCalibrate) {
-    if (valid && y == 1) {
-      key[0] = min(key[0], dkey(z));
+    if (valid && (invert ? y == 0 : y == 1)) {
+      key[0] = min(key[0], dkey(invert ? -z : z));
       if (nh > 0) key[1] = min(key[1], dkey(e[0]));
       if (nh > 1) key[2] = min(key[2], dkey(e[1]));
     }
@@ -662,7 +663,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
           cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
         }
       } else {
-        classify_row_smem<MODE, NHC>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+        classify_row_smem<MODE, NHC>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags, p.a.invert);
       }
     }
     tile = next;

@@ -72,10 +72,10 @@ __device__ __forceinline__ void fma2p(float& c0, float& c1, float a0, float a1, 
 template <int MODE>
 __device__ __forceinline__ void classify2(uint32_t* cnt, uint32_t (&key)[3], bool valid, int y,
                                           float z, const float* e, int nh, const float* tau,
-                                          unsigned int* flags) {
+                                          unsigned int* flags, int invert = 0) {
   if (MODE == kCalibrate) {
-    if (valid && y == 1) {
-      key[0] = min(key[0], dkey(z));
+    if (valid && (invert ? y == 0 : y == 1)) {
+      key[0] = min(key[0], dkey(invert ? -z : z));
       if (nh > 0) key[1] = min(key[1], dkey(e[0]));
       if (nh > 1) key[2] = min(key[2], dkey(e[1]));
     }
@@ -419,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
           cnt[0] += c0; cnt[1] += c1; cnt[2] += c2; cnt[3] += c3;
         }
       } else {
-        classify2<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags);
+        classify2<MODE>(cnt, key, valid, ythis, z, e, NH, p.a.tau, p.a.flags, p.a.invert);
       }
     }
     par ^= 1u;

@@ -131,6 +131,7 @@ struct nb_grid {
   int space_dim = 0, R = 0, frames = 1, device = 0;
   uint8_t* occ = nullptr;   // device copy of the grid
   int32_t* sat = nullptr;   // (R+1)^3 summed-area table (3D only)
+  uint8_t* blk = nullptr;   // 3D: any-occupied flag per 8^3-voxel block (plane labeller)
 };
 
 namespace nb {
@@ -175,6 +176,7 @@ struct FwdArgs {
   unsigned int* ticket_next;
   unsigned int* keys;
   unsigned int* flags;
+  int invert;  // kCalibrate: certainly-hit threshold (min of -z over negatives, nb_calibrate_inverted)
   TrainArgs tr;
 };
 
@@ -205,6 +207,7 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s);  // Adam + 
 cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, uint8_t* y,
                          cudaStream_t s);
 cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);
+cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s);
 
 // NCCL (dlopen'ed); all return 0 on success
 int comm_unique_id(uint8_t id[128]);

@@ -4,10 +4,17 @@
 //   point: f(x) = grid[min(R-1, floor(x R))...], 0 outside [0,1]^n;
 //   ray:   positive-length traversal of an occupied half-open voxel cell
 //          (Amanatides-Woo in fp64);
-//   box:   any occupied cell in [cell(lo), cell(hi)] via a summed-area table.
+//   box:   any occupied cell in [cell(lo), cell(hi)] via a summed-area table;
+//   plane: any occupied voxel whose closed cube has corners on both closed
+//          sides of n.(x - p0) = 0 (R19), corner values in fp64 exactly as the
+//          oracle writes them; 8^3 blocks whose corners are all clearly on
+//          one side (margin 1e-12) are skipped (a voxel cube lies inside its
+//          block's cube, so only blocks without a cut voxel are pruned).
 // This file is compiled with -fmad=false so every fp64 operation is rounded
 // exactly as written (no FMA contraction).
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "nb_internal.cuh"
 
@@ -94,6 +101,44 @@ __device__ int label_box(const nb_grid g, const float* r) {
   return c > 0;
 }
 
+__device__ int label_plane(const nb_grid g, const float* r) {
+  const int R = g.R, NB = (R + 7) / 8;
+  const double p0[3] = {r[0], r[1], r[2]}, nrm[3] = {r[3], r[4], r[5]};
+  auto sval = [&](int i, int j, int k) {
+    const double x = (double)i / R - p0[0];
+    const double y = (double)j / R - p0[1];
+    const double z = (double)k / R - p0[2];
+    return nrm[0] * x + nrm[1] * y + nrm[2] * z;
+  };
+  for (int bi = 0; bi < NB; ++bi)
+    for (int bj = 0; bj < NB; ++bj)
+      for (int bk = 0; bk < NB; ++bk) {
+        if (!g.blk[((size_t)bi * NB + bj) * NB + bk]) continue;
+        const int i0 = 8 * bi, j0 = 8 * bj, k0 = 8 * bk;
+        const int i1 = min(R, i0 + 8), j1 = min(R, j0 + 8), k1 = min(R, k0 + 8);
+        double mn = INFINITY, mx = -INFINITY;
+        for (int c = 0; c < 8; ++c) {
+          const double v = sval((c & 4) ? i1 : i0, (c & 2) ? j1 : j0, (c & 1) ? k1 : k0);
+          mn = v < mn ? v : mn;
+          mx = v > mx ? v : mx;
+        }
+        if (mn > 1e-12 || mx < -1e-12) continue;
+        for (int i = i0; i < i1; ++i)
+          for (int j = j0; j < j1; ++j)
+            for (int k = k0; k < k1; ++k) {
+              if (!g.occ[((size_t)i * R + j) * R + k]) continue;
+              int neg = 0, pos = 0;
+              for (int c = 0; c < 8; ++c) {
+                const double s = sval(i + ((c >> 2) & 1), j + ((c >> 1) & 1), k + (c & 1));
+                if (s <= 0.0) neg = 1;
+                if (s >= 0.0) pos = 1;
+              }
+              if (neg && pos) return 1;
+            }
+      }
+  return 0;
+}
+
 __global__ void k_label(const nb_grid g, int kind, const float* __restrict__ q, int64_t n,
                         uint8_t* __restrict__ y) {
   const int nf = kind == NB_POINT ? g.space_dim : 2 * g.space_dim;
@@ -104,9 +149,33 @@ __global__ void k_label(const nb_grid g, int kind, const float* __restrict__ q, 
     int v = 0;
     if (kind == NB_POINT) v = label_point(g, r);
     else if (kind == NB_RAY) v = label_ray(g, r);
+    else if (kind == NB_PLANE) v = label_plane(g, r);
     else v = label_box(g, r);
     y[i] = (uint8_t)v;
   }
+}
+
+__global__ void k_blk_build(const uint8_t* __restrict__ occ, int R, uint8_t* __restrict__ blk) {
+  const int NB = (R + 7) / 8;
+  const size_t nb3 = (size_t)NB * NB * NB;
+  for (size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x; b < nb3;
+       b += (size_t)gridDim.x * blockDim.x) {
+    const int bi = (int)(b / ((size_t)NB * NB)), bj = (int)((b / NB) % NB), bk = (int)(b % NB);
+    uint8_t any = 0;
+    for (int i = 8 * bi; i < min(R, 8 * bi + 8); ++i)
+      for (int j = 8 * bj; j < min(R, 8 * bj + 8); ++j)
+        for (int k = 8 * bk; k < min(R, 8 * bk + 8); ++k) any |= occ[((size_t)i * R + j) * R + k];
+    blk[b] = any ? 1 : 0;
+  }
+}
+
+cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s) {
+  const int NB = (g->R + 7) / 8;
+  const size_t nb3 = (size_t)NB * NB * NB;
+  cudaError_t e = cudaMalloc((void**)&g->blk, nb3);
+  if (e != cudaSuccess) return e;
+  k_blk_build<<<(unsigned)std::min<size_t>((nb3 + 255) / 256, 4096), 256, 0, s>>>(g->occ, g->R, g->blk);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, uint8_t* y,

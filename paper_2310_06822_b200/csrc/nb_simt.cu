@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
       }
     } else {
       int y = valid ? a.y[i] : 0;
-      classify_row<MODE>(acc, valid, y, z, e, s.nh, a.tau, a.flags);
+      classify_row<MODE>(acc, valid, y, z, e, s.nh, a.tau, a.flags, a.invert);
     }
   }
   if (MODE != kForward) flush_warp<MODE>(acc, s.nh, a.counts, a.keys);

@@ -800,3 +800,115 @@ def test_bf16_sine_pe_train_step_gradient_parity(name, width, layers, pe, n):
     m2.set_params(m.get_params())
     qq = cuda(q[:1000])
     assert torch.equal(m.forward(qq), m2.forward(qq))
+
+
+# ---------------------------------------------------------------- NEXT-3: planes, OccNet ablation
+def _plane_cfg():
+    import dataclasses
+    return dataclasses.replace(nbgen.CONFIGS["c3"], name="c3plane", kind="plane")
+
+
+def test_gpu_plane_labeller_bit_exact():
+    """Plane queries (R19): the GPU labeller (block-pruned fp64 corner
+    test) equals the oracle's voxel scan, including planes through voxel
+    faces and edges (closed-side ties)."""
+    cfg = _plane_cfg()
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 6000).numpy()
+    R = nbgen.CONFIGS["c3"].grid["R"]
+    edge = []
+    for k in (0, 1, 17, 32, 63, 64):   # axis-aligned planes on grid faces
+        for ax in range(3):
+            p0 = [0.5, 0.5, 0.5]
+            p0[ax] = k / R
+            nrm = [0.0, 0.0, 0.0]
+            nrm[ax] = 1.0
+            edge.append(p0 + nrm)
+    edge.append([0.25, 0.25, 0.25, 0.70710678, 0.70710678, 0.0])
+    q = np.concatenate([q, np.array(edge, np.float32)], 0)
+    grid = grid_of(nbgen.CONFIGS["c3"])
+    y_ora = oracle.label(grid, 3, "plane", q)
+    g = nb.Grid(torch.from_numpy(grid), 3, DEV)
+    y_gpu = g.label("plane", cuda(torch.from_numpy(q))).cpu().numpy()
+    assert np.array_equal(y_gpu, y_ora)
+    assert 0.05 < y_ora.mean() < 0.99
+
+
+def test_bf16_plane_queries_forward_and_counts():
+    """Plane records (p0, unit normal) through the fused kernels (the encoder
+    is kind-agnostic: 6 floats like a ray): sigmoid within 2e-2 of fp64 and
+    counts equal to the bf16-emulating oracle outside the band."""
+    cfg = _plane_cfg()
+    n = (1 << 14) + 21
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    grid = grid_of(nbgen.CONFIGS["c3"])
+    y = oracle.label(grid, 3, "plane", q.numpy())
+    th = scaled_params(nbgen.CONFIGS["c3"], 4)
+    m = nb.Model(nb.Desc("plane", 3, 128, 4, (), "bf16"), DEV)
+    m.set_params(th)
+    qd, yd = cuda(q), cuda(y)
+    z, p = m.forward(qd, prob=True)
+    a = oracle.make_arch(6, 128, 4)
+    zr = oracle.forward(a, th.double().numpy(), q.numpy())[:, 0]
+    assert np.max(np.abs(p.cpu().double().numpy() - 1 / (1 + np.exp(-zr)))) <= 2e-2
+    tau = m.calibrate(qd, yd).numpy()
+    ze = oracle.forward(a, th.double().numpy(), q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    keep = ~band_mask(z.cpu().double().numpy(), tau, ze, te)
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    assert all(cg[k] == co[k] for k in ("tp", "fp", "fn", "tn")), (cg, co)
+    assert m.score(qd, yd)["fn"] == 0
+
+
+def test_symmetric_loss_ablation_leaves_false_negatives():
+    """The OccNet-style symmetric loss (alpha = beta = 1) trained
+    like c1 misses positives at the rounding rule z >= 0; the
+    asymmetric ramp of Eq. (1) leaves fewer, and calibration (R21) removes
+    them for both."""
+    cfg = nbgen.CONFIGS["c1"]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, cfg.n_eval)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    fn = {}
+    for mode in ("symmetric", "asymmetric"):
+        m = nb.Model(desc_of(cfg), DEV)
+        m.set_params(nbgen.init_params(cfg))
+        T = cfg.train_steps
+        for t in range(T):
+            sl = slice((t % 16) * 4096, (t % 16 + 1) * 4096)
+            m.train_step(qd[sl], yd[sl], alpha=1.0 if mode == "symmetric" else nb.alpha(t, T), beta=1.0)
+        m.set_thresholds([0.0])
+        fn[mode] = m.score(qd, yd)["fn"]
+        m.calibrate(qd, yd)
+        assert m.score(qd, yd)["fn"] == 0
+    assert fn["symmetric"] > 0 and fn["asymmetric"] < fn["symmetric"], fn
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+def test_inverted_certainly_hit_bounding(name):
+    """Inverted bounding (R43): trained with the asymmetry flipped
+    (FP weight ramped, FN weight 1), nb_calibrate_inverted's threshold is the
+    next float above the largest negative logit: FP = 0 on the set, equal to
+    the oracle's (bf16-emulating for bf16 nets) max over negatives outside
+    the band."""
+    cfg = nbgen.CONFIGS[name]
+    n = 1 << 14
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(nbgen.init_params(cfg))
+    B = 4096
+    for t in range(30):
+        sl = slice((t % 4) * B, (t % 4 + 1) * B)
+        m.train_step(qd[sl], yd[sl], alpha=1.0, beta=nb.alpha(t, 30), lr=1e-3)
+    tau = float(m.calibrate_inverted(qd, yd)[0])
+    c = m.score(qd, yd)
+    assert c["fp"] == 0 and c["tp"] + c["fn"] == int(y.sum())
+    z = m.forward(qd).cpu().double().numpy()[:, 0]
+    zmax = z[y == 0].max()
+    assert tau == np.nextafter(np.float32(zmax), np.float32(np.inf))
+    mode = oracle.FP64 if cfg.precision == "fp32" else oracle.BF16_EMU
+    zo = oracle.forward(oracle.arch_of(cfg), m.get_params().double().numpy(), q.numpy(), mode)[:, 0]
+    tol = 1e-5 * max(1.0, abs(zmax)) if cfg.precision == "fp32" else 1e-3 + 2e-2 * abs(zmax)
+    assert abs(zo[y == 0].max() - zmax) <= tol
