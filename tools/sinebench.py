@@ -13,10 +13,15 @@ import torch
 import nbgen
 import paper_2310_06822_b200 as nb
 
+if os.environ.get("NB_LIB", ""):  # measurement variant (build.py --name=...)
+    nb.LIB_PATH = os.path.join(os.path.dirname(nb.LIB_PATH), f"libnb_{os.environ['NB_LIB']}.so")
+
 logn = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 n = 1 << logn
 cases = [("c2", 64, 4, "relu", 0), ("c2", 64, 4, "sine", 0), ("c3", 128, 4, "relu", 0),
          ("c3", 128, 4, "sine", 0), ("c1", 128, 3, "sine", 8), ("c1", 128, 3, "relu", 8)]
+if os.environ.get("NB_SINE_ONLY"):
+    cases = [c for c in cases if c[3] == "sine"]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name, W, L, act, pe in cases:
     cfg = nbgen.CONFIGS[name]
