@@ -214,10 +214,19 @@ def make_grid(cfg: Config) -> torch.Tensor:
 # per Suppl. §3.2).  Records are fp32 rows of record_floats values.
 # --------------------------------------------------------------------------
 DRAWS_PER_ROW = {"point": None, "ray": 5, "box": 6, "plane": 5}
+DRAWS_PER_ROW_2D = {"ray": 3, "box": 4, "plane": 3}  # 2D rays / boxes / lines
 
 
 def _draws_per_row(cfg: Config) -> int:
-    return cfg.space_dim if cfg.kind == "point" else DRAWS_PER_ROW[cfg.kind]
+    if cfg.kind == "point":
+        return cfg.space_dim
+    return DRAWS_PER_ROW_2D[cfg.kind] if cfg.space_dim == 2 else DRAWS_PER_ROW[cfg.kind]
+
+
+def _unit_dirs_2d(u_phi: torch.Tensor) -> torch.Tensor:
+    """Uniform directions on the unit circle."""
+    phi = 2.0 * math.pi * u_phi.double()
+    return torch.stack([torch.cos(phi), torch.sin(phi)], dim=1)
 
 
 def _unit_dirs(u_z: torch.Tensor, u_phi: torch.Tensor) -> torch.Tensor:
@@ -235,6 +244,23 @@ def make_queries(cfg: Config, tag: int, row0: int, n: int, device="cpu") -> torc
     u = u32f(draws(key, row0 * D, n * D, device)).view(n, D)
     if cfg.kind == "point":
         return u.contiguous()
+    if cfg.space_dim == 2:  # 4-float records: origin on the square's boundary + direction,
+        if cfg.kind == "ray":  # lo/hi corners, or a line's point + unit normal
+            edge = torch.clamp((u[:, 0].double() * 4.0).floor().long(), max=3)
+            axis, side = edge % 2, (edge // 2).double()
+            o = torch.empty(n, 2, dtype=torch.float64, device=device)
+            for a in range(2):
+                m = axis == a
+                o[m, a] = side[m]
+                o[m, 1 - a] = u[:, 1].double()[m]
+            return torch.cat([o, _unit_dirs_2d(u[:, 2])], 1).to(torch.float32).contiguous()
+        if cfg.kind == "box":
+            lo = u[:, 0:2]
+            e = 0.005 + 0.095 * u[:, 2:4].double()
+            hi = torch.clamp(lo.double() + e, max=1.0).to(torch.float32)
+            return torch.cat([lo, hi], 1).contiguous()
+        if cfg.kind == "plane":
+            return torch.cat([u[:, 0:2].double(), _unit_dirs_2d(u[:, 2])], 1).to(torch.float32).contiguous()
     if cfg.kind == "ray":
         assert cfg.space_dim == 3
         face = torch.clamp((u[:, 0].double() * 6.0).floor().long(), max=5)

@@ -238,11 +238,151 @@ static int plane_brute(const uint8_t* g, int32_t R, const double* p0, const doub
   return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* 2D rays, boxes and lines: the readings R15-R19 with
+ * pixels instead of voxels; grid [R][R], axis 0 slowest.                  */
+static int occ2(const uint8_t* g, int32_t R, int i, int j) { return g[(int64_t)i * R + j] != 0; }
+
+static int ray2_clip(const double* o, const double* d, double* s_in, double* s_out) {
+  double a = 0.0, b = INFINITY;
+  for (int j = 0; j < 2; ++j) {
+    if (d[j] == 0.0) {
+      if (o[j] < 0.0 || o[j] > 1.0) return 0;
+      continue;
+    }
+    double t0 = (0.0 - o[j]) / d[j], t1 = (1.0 - o[j]) / d[j];
+    if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+    if (t0 > a) a = t0;
+    if (t1 < b) b = t1;
+  }
+  *s_in = a; *s_out = b;
+  return b > a;
+}
+
+static int ray2_dda(const uint8_t* g, int32_t R, const double* o, const double* d) {
+  double s_in, s_out;
+  if (!ray2_clip(o, d, &s_in, &s_out)) return 0;
+  int idx[2], step[2];
+  double tmax[2];
+  for (int j = 0; j < 2; ++j) {
+    double pr = (o[j] + s_in * d[j]) * (double)R;
+    int64_t i = (int64_t)floor(pr);
+    if ((double)i == pr && d[j] < 0.0) i -= 1;
+    if (i < 0) i = 0;
+    if (i > R - 1) i = R - 1;
+    idx[j] = (int)i;
+    if (d[j] > 0.0) { step[j] = 1; tmax[j] = ((double)(idx[j] + 1) / (double)R - o[j]) / d[j]; }
+    else if (d[j] < 0.0) { step[j] = -1; tmax[j] = ((double)idx[j] / (double)R - o[j]) / d[j]; }
+    else { step[j] = 0; tmax[j] = INFINITY; }
+  }
+  double s = s_in;
+  for (;;) {
+    int a = tmax[1] < tmax[0] ? 1 : 0;
+    double s_next = tmax[a] < s_out ? tmax[a] : s_out;
+    if (s_next > s && occ2(g, R, idx[0], idx[1])) return 1;
+    if (tmax[a] >= s_out) return 0;
+    s = s_next;
+    idx[a] += step[a];
+    if (idx[a] < 0 || idx[a] >= R) return 0;
+    tmax[a] = (step[a] > 0 ? ((double)(idx[a] + 1) / (double)R - o[a])
+                           : ((double)idx[a] / (double)R - o[a])) / d[a];
+  }
+}
+
+static int ray2_brute(const uint8_t* g, int32_t R, const double* o, const double* d) {
+  double s_in, s_out;
+  if (!ray2_clip(o, d, &s_in, &s_out)) return 0;
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) {
+      if (!occ2(g, R, i, j)) continue;
+      int c[2] = {i, j};
+      double a = s_in, b = s_out;
+      int ok = 1;
+      for (int ax = 0; ax < 2 && ok; ++ax) {
+        double lo = (double)c[ax] / (double)R, hi = (double)(c[ax] + 1) / (double)R;
+        if (d[ax] == 0.0) {
+          if (cell_index(o[ax], R) != c[ax]) ok = 0;
+          continue;
+        }
+        double t0 = (lo - o[ax]) / d[ax], t1 = (hi - o[ax]) / d[ax];
+        if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+        if (t0 > a) a = t0;
+        if (t1 < b) b = t1;
+      }
+      if (ok && b > a) return 1;
+    }
+  return 0;
+}
+
+static int box2_cells(const double* lo, const double* hi, int32_t R, int* a, int* b) {
+  for (int j = 0; j < 2; ++j) {
+    double l = lo[j] < 0.0 ? 0.0 : lo[j];
+    double h = hi[j] > 1.0 ? 1.0 : hi[j];
+    if (!(h >= l)) return 0;
+    a[j] = cell_index(l, R);
+    b[j] = cell_index(h, R);
+  }
+  return 1;
+}
+
+/* 2D summed-area table S[i][j] = occupied pixels (i' < i, j' < j). */
+static void sat2_build(const uint8_t* g, int32_t R, int32_t* S) {
+  const int64_t R1 = R + 1;
+  memset(S, 0, sizeof(int32_t) * R1 * R1);
+  for (int i = 1; i <= R; ++i)
+    for (int j = 1; j <= R; ++j)
+      S[i * R1 + j] = occ2(g, R, i - 1, j - 1) + S[(i - 1) * R1 + j] + S[i * R1 + j - 1] -
+                      S[(i - 1) * R1 + j - 1];
+}
+
+static int box2_sat(const int32_t* S, int32_t R, const double* lo, const double* hi) {
+  int a[2], b[2];
+  if (!box2_cells(lo, hi, R, a, b)) return 0;
+  const int64_t R1 = R + 1, i0 = a[0], i1 = b[0] + 1, j0 = a[1], j1 = b[1] + 1;
+  return (S[i1 * R1 + j1] - S[i0 * R1 + j1] - S[i1 * R1 + j0] + S[i0 * R1 + j0]) > 0;
+}
+
+static int box2_scan(const uint8_t* g, int32_t R, const double* lo, const double* hi) {
+  int a[2], b[2];
+  if (!box2_cells(lo, hi, R, a, b)) return 0;
+  for (int i = a[0]; i <= b[0]; ++i)
+    for (int j = a[1]; j <= b[1]; ++j)
+      if (occ2(g, R, i, j)) return 1;
+  return 0;
+}
+
+/* line n.(x - p0) = 0 meets the closed square of an occupied pixel: its
+ * corners lie on both closed sides (R19 in 2D).                           */
+static int line2_scan_res(const uint8_t* g, int32_t R, int sub, const double* p0, const double* nrm) {
+  for (int i = 0; i < sub * R; ++i)
+    for (int j = 0; j < sub * R; ++j) {
+      if (!occ2(g, R, i / sub, j / sub)) continue;
+      int neg = 0, pos = 0;
+      for (int c = 0; c < 4; ++c) {
+        double x = (double)(i + ((c >> 1) & 1)) / ((double)sub * R) - p0[0];
+        double y = (double)(j + (c & 1)) / ((double)sub * R) - p0[1];
+        double sv = nrm[0] * x + nrm[1] * y;
+        if (sv <= 0.0) neg = 1;
+        if (sv >= 0.0) pos = 1;
+      }
+      if (neg && pos) return 1;
+    }
+  return 0;
+}
+
 static int label_one(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames, int32_t kind,
                      const float* r, const int32_t* S, int brute) {
   double v[8];
   int nf = (kind == ORA_POINT) ? sd : 2 * sd;
   for (int j = 0; j < nf; ++j) v[j] = (double)r[j];
+  if (sd == 2 && kind != ORA_POINT) {
+    switch (kind) {
+      case ORA_RAY: return brute ? ray2_brute(grid, R, v, v + 2) : ray2_dda(grid, R, v, v + 2);
+      case ORA_BOX: return brute ? box2_scan(grid, R, v, v + 2) : box2_sat(S, R, v, v + 2);
+      case ORA_PLANE: return line2_scan_res(grid, R, brute ? 2 : 1, v, v + 2);
+    }
+    return 0;
+  }
   switch (kind) {
     case ORA_POINT: return ora_indicator(grid, sd, R, frames, v);
     case ORA_RAY: return brute ? ray_brute(grid, R, v, v + 3) : ray_dda(grid, R, v, v + 3);
@@ -255,12 +395,15 @@ static int label_one(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames,
 static int label_impl(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames, int32_t kind,
                       const float* q, int64_t n, uint8_t* y, int brute) {
   if (kind == ORA_POINT && !(sd >= 2 && sd <= 4)) return -1;
-  if (kind != ORA_POINT && sd != 3) return -1;
+  if (kind != ORA_POINT && sd != 3 && sd != 2) return -1;
   int nf = (kind == ORA_POINT) ? sd : 2 * sd;
   int32_t* S = NULL;
-  if (kind == ORA_BOX && !brute) {
+  if (kind == ORA_BOX && !brute && sd == 3) {
     S = (int32_t*)malloc(sizeof(int32_t) * (size_t)(R + 1) * (R + 1) * (R + 1));
     ora_sat_build(grid, R, S);
+  } else if (kind == ORA_BOX && !brute) {
+    S = (int32_t*)malloc(sizeof(int32_t) * (size_t)(R + 1) * (R + 1));
+    sat2_build(grid, R, S);
   }
 #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t i = 0; i < n; ++i)

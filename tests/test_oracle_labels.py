@@ -168,3 +168,69 @@ def test_plane_scan_equals_subdivision():
     b = oracle.label(g, 3, "plane", q, brute=True)
     assert (a == b).all()
     assert 0 < a.mean() < 1
+
+
+# ---------------------------------------------------------------- 2D rays, boxes, lines (NEXT-3)
+def _cfg2(kind):
+    import dataclasses
+    return dataclasses.replace(nbgen.CONFIGS["c1"], kind=kind)
+
+
+def rand_grid2(R, p, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.random((R, R)) < p).astype(np.uint8)
+
+
+@pytest.mark.parametrize("R,p,seed", [(4, 0.2, 0), (8, 0.1, 1), (8, 0.4, 2), (16, 0.05, 3)])
+def test_ray2_dda_equals_brute_force(R, p, seed):
+    """2D DDA (R16 with pixels) == slab test of every occupied pixel, on
+    random rays plus rays along pixel edges and through pixel corners."""
+    g = rand_grid2(R, p, seed)
+    q = nbgen.make_queries(_cfg2("ray"), nbgen.TAG_EVAL, seed * 1000, 3000).numpy()
+    edge = []
+    for k in range(R + 1):
+        edge.append([k / R, 0.0, 0.0, 1.0])
+        edge.append([0.0, k / R, 1.0, 0.0])
+        edge.append([0.0, k / R, 0.70710678, 0.70710678])
+        edge.append([1.0, k / R, -1.0, 0.0])
+    q = np.concatenate([q, np.array(edge, np.float32)])
+    assert np.array_equal(oracle.label(g, 2, "ray", q), oracle.label(g, 2, "ray", q, brute=True))
+
+
+def test_ray2_full_and_empty_grid():
+    q = nbgen.make_queries(_cfg2("ray"), nbgen.TAG_EVAL, 0, 2000).numpy()
+    assert oracle.label(np.zeros((8, 8), np.uint8), 2, "ray", q).sum() == 0
+    # a ray entering through the left edge crosses a pixel with positive length
+    rng = np.random.default_rng(3)
+    th = rng.uniform(-1.3, 1.3, 500)
+    inward = np.stack([np.zeros(500), rng.random(500), np.cos(th), np.sin(th)], 1).astype(np.float32)
+    assert oracle.label(np.ones((8, 8), np.uint8), 2, "ray", inward).all()
+    # and one leaving it (pointing away from the square) crosses none
+    assert oracle.label(np.ones((8, 8), np.uint8), 2, "ray", inward * np.array([1, 1, -1, 1], np.float32)).sum() == 0
+
+
+@pytest.mark.parametrize("R,p,seed", [(8, 0.05, 0), (16, 0.02, 1), (32, 0.01, 2)])
+def test_box2_sat_equals_scan_and_contains_pixel(R, p, seed):
+    g = rand_grid2(R, p, seed)
+    q = nbgen.make_queries(_cfg2("box"), nbgen.TAG_EVAL, seed, 5000).numpy()
+    y = oracle.label(g, 2, "box", q)
+    assert np.array_equal(y, oracle.label(g, 2, "box", q, brute=True))
+    # a box containing the centre of an occupied pixel is positive (R17)
+    occ = np.argwhere(g)
+    c = (occ + 0.5) / R
+    boxes = np.concatenate([c - 1e-3, c + 1e-3], 1).astype(np.float32)
+    assert oracle.label(g, 2, "box", boxes).all()
+
+
+@pytest.mark.parametrize("R,p,seed", [(8, 0.1, 0), (16, 0.03, 1)])
+def test_line2_scan_equals_subdivision(R, p, seed):
+    """2D lines (R19 with pixels): the corner test on occupied pixels equals
+    the same test on their 2x2 children (a convex square is cut iff a child is)."""
+    g = rand_grid2(R, p, seed)
+    q = nbgen.make_queries(_cfg2("plane"), nbgen.TAG_EVAL, seed, 3000).numpy()
+    edge = np.array([[k / R, 0.5, 1.0, 0.0] for k in range(R + 1)] +
+                    [[0.5, k / R, 0.0, 1.0] for k in range(R + 1)], np.float32)
+    q = np.concatenate([q, edge])
+    y = oracle.label(g, 2, "plane", q)
+    assert np.array_equal(y, oracle.label(g, 2, "plane", q, brute=True))
+    assert 0 < y.mean() < 1
