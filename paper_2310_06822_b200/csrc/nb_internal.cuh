@@ -208,6 +208,7 @@ cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, 
                          cudaStream_t s);
 cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s);
+cudaError_t launch_sat2_build(nb_grid* g, cudaStream_t s);
 
 // NCCL (dlopen'ed); all return 0 on success
 int comm_unique_id(uint8_t id[128]);

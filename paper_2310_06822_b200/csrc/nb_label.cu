@@ -139,6 +139,85 @@ __device__ int label_plane(const nb_grid g, const float* r) {
   return 0;
 }
 
+// ---- 2D rays, boxes and lines (pixel readings; the same fp64 expressions as
+// the oracle's ray2_dda / box2_sat / line2_scan_res)
+__device__ int label_ray2(const nb_grid g, const float* r) {
+  const int R = g.R;
+  const double o[2] = {r[0], r[1]}, d[2] = {r[2], r[3]};
+  double s0 = 0.0, s1 = INFINITY;
+  for (int a = 0; a < 2; ++a) {
+    if (d[a] == 0.0) {
+      if (o[a] < 0.0 || o[a] > 1.0) return 0;
+    } else {
+      double ta = (0.0 - o[a]) / d[a], tb = (1.0 - o[a]) / d[a];
+      double lo = ta < tb ? ta : tb, hi = ta < tb ? tb : ta;
+      s0 = lo > s0 ? lo : s0;
+      s1 = hi < s1 ? hi : s1;
+    }
+  }
+  if (!(s1 > s0)) return 0;
+  int cell[2], dir[2];
+  double next[2];
+  for (int a = 0; a < 2; ++a) {
+    const double xr = (o[a] + s0 * d[a]) * (double)R;
+    long long c = (long long)floor(xr);
+    if (d[a] < 0.0 && (double)c == xr) c -= 1;
+    c = c < 0 ? 0 : (c > R - 1 ? R - 1 : c);
+    cell[a] = (int)c;
+    dir[a] = d[a] > 0.0 ? 1 : (d[a] < 0.0 ? -1 : 0);
+    if (dir[a] > 0) next[a] = ((double)(cell[a] + 1) / (double)R - o[a]) / d[a];
+    else if (dir[a] < 0) next[a] = ((double)cell[a] / (double)R - o[a]) / d[a];
+    else next[a] = INFINITY;
+  }
+  double s = s0;
+  while (true) {
+    const int a = next[1] < next[0] ? 1 : 0;
+    const double e = next[a] < s1 ? next[a] : s1;
+    if (e > s && g.occ[(size_t)cell[0] * R + cell[1]]) return 1;
+    if (!(next[a] < s1)) return 0;
+    s = e;
+    cell[a] += dir[a];
+    if (cell[a] < 0 || cell[a] >= R) return 0;
+    next[a] = (dir[a] > 0 ? ((double)(cell[a] + 1) / (double)R - o[a])
+                          : ((double)cell[a] / (double)R - o[a])) / d[a];
+  }
+}
+
+__device__ int label_box2(const nb_grid g, const float* r) {
+  const int R = g.R;
+  int a[2], b[2];
+  for (int j = 0; j < 2; ++j) {
+    double lo = r[j], hi = r[2 + j];
+    lo = lo < 0.0 ? 0.0 : lo;
+    hi = hi > 1.0 ? 1.0 : hi;
+    if (!(hi >= lo)) return 0;
+    a[j] = cell_of(lo, R);
+    b[j] = cell_of(hi, R) + 1;
+  }
+  const size_t R1 = (size_t)R + 1;
+  auto S = [&](int i, int j) -> long long { return g.sat[(size_t)i * R1 + j]; };
+  return (S(b[0], b[1]) - S(a[0], b[1]) - S(b[0], a[1]) + S(a[0], a[1])) > 0;
+}
+
+__device__ int label_line2(const nb_grid g, const float* r) {
+  const int R = g.R;
+  const double p0[2] = {r[0], r[1]}, nrm[2] = {r[2], r[3]};
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) {
+      if (!g.occ[(size_t)i * R + j]) continue;
+      int neg = 0, pos = 0;
+      for (int c = 0; c < 4; ++c) {
+        const double x = (double)(i + ((c >> 1) & 1)) / ((double)1 * R) - p0[0];
+        const double y = (double)(j + (c & 1)) / ((double)1 * R) - p0[1];
+        const double sv = nrm[0] * x + nrm[1] * y;
+        if (sv <= 0.0) neg = 1;
+        if (sv >= 0.0) pos = 1;
+      }
+      if (neg && pos) return 1;
+    }
+  return 0;
+}
+
 __global__ void k_label(const nb_grid g, int kind, const float* __restrict__ q, int64_t n,
                         uint8_t* __restrict__ y) {
   const int nf = kind == NB_POINT ? g.space_dim : 2 * g.space_dim;
@@ -148,6 +227,7 @@ __global__ void k_label(const nb_grid g, int kind, const float* __restrict__ q, 
     for (int j = 0; j < nf; ++j) r[j] = q[i * nf + j];
     int v = 0;
     if (kind == NB_POINT) v = label_point(g, r);
+    else if (g.space_dim == 2) v = kind == NB_RAY ? label_ray2(g, r) : (kind == NB_BOX ? label_box2(g, r) : label_line2(g, r));
     else if (kind == NB_RAY) v = label_ray(g, r);
     else if (kind == NB_PLANE) v = label_plane(g, r);
     else v = label_box(g, r);
@@ -175,6 +255,33 @@ cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s) {
   cudaError_t e = cudaMalloc((void**)&g->blk, nb3);
   if (e != cudaSuccess) return e;
   k_blk_build<<<(unsigned)std::min<size_t>((nb3 + 255) / 256, 4096), 256, 0, s>>>(g->occ, g->R, g->blk);
+  return cudaGetLastError();
+}
+
+__global__ void k_sat2(const uint8_t* __restrict__ occ, int R, int32_t* __restrict__ S) {
+  // one thread per row prefix, then per column: (R+1)^2 table with a zero border
+  const size_t R1 = (size_t)R + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += gridDim.x * blockDim.x) {
+    int32_t acc = 0;
+    S[(size_t)i * R1] = 0;
+    for (int j = 1; j <= R; ++j) {
+      if (i > 0) acc += occ[(size_t)(i - 1) * R + (j - 1)];
+      S[(size_t)i * R1 + j] = acc;
+    }
+  }
+}
+__global__ void k_sat2_cols(int R, int32_t* __restrict__ S) {
+  const size_t R1 = (size_t)R + 1;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= R; j += gridDim.x * blockDim.x)
+    for (int i = 1; i <= R; ++i) S[(size_t)i * R1 + j] += S[(size_t)(i - 1) * R1 + j];
+}
+
+cudaError_t launch_sat2_build(nb_grid* g, cudaStream_t s) {
+  const int R = g->R;
+  cudaError_t e = cudaMalloc((void**)&g->sat, sizeof(int32_t) * (size_t)(R + 1) * (R + 1));
+  if (e != cudaSuccess) return e;
+  k_sat2<<<(R + 256) / 256, 256, 0, s>>>(g->occ, R, g->sat);
+  k_sat2_cols<<<(R + 256) / 256, 256, 0, s>>>(R, g->sat);
   return cudaGetLastError();
 }
 

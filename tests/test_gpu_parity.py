@@ -912,3 +912,34 @@ def test_inverted_certainly_hit_bounding(name):
     zo = oracle.forward(oracle.arch_of(cfg), m.get_params().double().numpy(), q.numpy(), mode)[:, 0]
     tol = 1e-5 * max(1.0, abs(zmax)) if cfg.precision == "fp32" else 1e-3 + 2e-2 * abs(zmax)
     assert abs(zo[y == 0].max() - zmax) <= tol
+
+
+@pytest.mark.parametrize("kind", ["ray", "box", "plane"])
+def test_gpu_2d_labellers_bit_exact_and_kernels(kind):
+    """2D rays, boxes and lines (4-float records, NEXT-3) on the c1 grid: the
+    GPU labeller equals the oracle (pixel readings of R15-R19), and a bf16
+    4 -> 64 x 3 net scores them with counts equal to the bf16-emulating
+    oracle outside the band and FN = 0 after calibration."""
+    import dataclasses
+    cfg = dataclasses.replace(nbgen.CONFIGS["c1"], kind=kind)
+    n = (1 << 14) + 3
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    grid = grid_of(nbgen.CONFIGS["c1"])
+    y = oracle.label(grid, 2, kind, q.numpy())
+    g = nb.Grid(torch.from_numpy(grid), 2, DEV)
+    assert np.array_equal(g.label(kind, cuda(q)).cpu().numpy(), y)
+    assert 0.02 < y.mean() < 0.98
+    a = oracle.make_arch(4, 64, 3)
+    th = torch.from_numpy(np.random.default_rng(2).normal(size=oracle.num_params(a)) * 0.15).float()
+    m = nb.Model(nb.Desc(kind, 2, 64, 3, (), "bf16"), DEV)
+    m.set_params(th)
+    qd, yd = cuda(q), cuda(y)
+    tau = m.calibrate(qd, yd).numpy()
+    assert m.score(qd, yd)["fn"] == 0
+    zg = m.forward(qd).cpu().double().numpy()
+    ze = oracle.forward(a, th.double().numpy(), q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    keep = ~band_mask(zg, tau, ze, te)
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    assert all(cg[k] == co[k] for k in ("tp", "fp", "fn", "tn")), (cg, co)
