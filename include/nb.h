@@ -256,6 +256,18 @@ nb_status nb_schedule_init(nb_schedule* s, int32_t space_dim, int64_t step_every
 /* Report one finished step's batch FN; updates alpha, beta, lambda, stop.   */
 nb_status nb_schedule_after_step(nb_schedule* s, uint64_t batch_fn);
 
+/* ---- neural bounding hierarchies (§3.2) ------ */
+/* Node i bounds the union of the indicators below it; parent[0] = -1 (root),
+ * 0 <= parent[i] < i.  A record is predicted positive iff some root-to-leaf
+ * path has every node predicting positive (each node's calibrated
+ * predictor, exit heads included; R45).  Evaluated with pruning:
+ * a node runs only on the rows its parent passed (gather -> the node's fused
+ * forward -> compaction).  Writes tp/fp/fn/tn of that predictor against y
+ * (exit_hist, nonfinite = 0).  All nodes on one device with the same record
+ * layout, no communicator; n < 2^31.  Synchronises `stream` once per node.  */
+nb_status nb_hier_score(nb_model* const* nodes, int32_t n_nodes, const int32_t* parent, const float* q,
+                        const uint8_t* y, int64_t n, nb_counts* out, void* stream);
+
 /* ---- ground-truth labeller (harness support, not a hot-path row) ----------- */
 /* Occupancy grid uint8 host array, row-major, axis 0 slowest; 4D grids are
  * [frames][R][R][R].  Builds a summed-area table on the device for boxes.   */

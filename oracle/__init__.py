@@ -237,6 +237,34 @@ class PaperSchedule:
         self.stop = self.stable >= 6 or self.step >= self.max_steps
 
 
+def hier_combine(parent, passes) -> np.ndarray:
+    """Neural bounding hierarchy (§3.2; R45): a record is
+    positive iff some root-to-leaf path has every node passing.  parent[0] =
+    -1, parent[i] < i; passes: bool [nodes][n].  Forward propagation of
+    "every node on the path so far passes", then OR over the leaves."""
+    passes = np.asarray(passes, bool)
+    ok = np.zeros_like(passes)
+    leaf = np.ones(len(parent), bool)
+    for i, p in enumerate(parent):
+        ok[i] = passes[i] if p < 0 else (ok[p] & passes[i])
+        if p >= 0:
+            leaf[p] = False
+    return np.any(ok[leaf], axis=0)
+
+
+def hier_predict(archs, thetas, taus, parent, q, mode=FP64) -> np.ndarray:
+    """Each node's calibrated predictor [e_k >= tau_k][z >= tau] on every
+    record (no pruning: the definition), combined by hier_combine."""
+    passes = []
+    for a, th, tau in zip(archs, thetas, taus):
+        z = forward(a, th, q, mode)
+        ok = z[:, 0] >= tau[0]
+        for k in range(a.n_heads):
+            ok &= z[:, 1 + k] >= tau[1 + k]
+        passes.append(ok)
+    return hier_combine(parent, passes)
+
+
 def alpha(t, T) -> float:
     return float(lib().ora_alpha(t, T))
 

@@ -115,6 +115,7 @@ SIGNATURES = {
     "nb_calibrate": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_calibrate_inverted": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "nb_hier_score": (C.c_int, [_P, _I32, _P, _P, _P, _I64, _P, _P]),
     "nb_score_host": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score_async": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
@@ -383,6 +384,18 @@ class Model:
         if st is not None:
             return dict(loss=st.loss, tp=st.tp, fp=st.fp, fn=st.fn, tn=st.tn)
         return None
+
+
+def hier_score(nodes, parent, q: torch.Tensor, y: torch.Tensor) -> dict:
+    """Neural bounding hierarchy (nb_hier_score): counts of the
+    predictor "some root-to-leaf path passes every node"."""
+    dev = nodes[0].device
+    arr = (C.c_void_p * len(nodes))(*[m._h.value if isinstance(m._h, C.c_void_p) else m._h for m in nodes])
+    par = (C.c_int32 * len(parent))(*parent)
+    c = _Counts()
+    _check(lib().nb_hier_score(arr, len(nodes), par, nodes[0]._q(q), _dev_ptr(y, torch.uint8, dev, "y"),
+                               q.shape[0], C.byref(c), _stream(dev)), "nb_hier_score")
+    return c.as_dict()
 
 
 class Grid:

@@ -35,6 +35,7 @@ SOURCES = {
     "nb_train_tc2.cu": [],
     "nb_train_fused.cu": [],
     "nb_fwd_exit.cu": [],
+    "nb_hier.cu": [],
     "nb_fwd_tc_ext32.cu": [],
     "nb_fwd_tc_ext64.cu": [],
     "nb_fwd_tc_ext128.cu": [],

@@ -815,6 +815,33 @@ nb_status nb_comm_version(int32_t* v) {
   return NB_OK;
 }
 
+// Node forward for the hierarchy: the model's fused kernel in forward mode.
+static cudaError_t hier_forward(const nb_model* m, const float* q, int64_t n, float* logits, cudaStream_t s) {
+  FwdArgs a = base_args(m, q, nullptr, n);
+  a.logits = logits;
+  return launch_forward_any(m, kForward, a, s);
+}
+
+nb_status nb_hier_score(nb_model* const* nodes, int32_t n_nodes, const int32_t* parent, const float* q,
+                        const uint8_t* y, int64_t n, nb_counts* out, void* stream) {
+  if (!nodes || n_nodes < 1 || !parent || !out || n < 0 || n > INT32_MAX || (n > 0 && (!q || !y)))
+    return set_error("bad argument"), NB_E_ARG;
+  if (parent[0] != -1) return set_error("parent[0] must be -1 (root)"), NB_E_ARG;
+  for (int i = 0; i < n_nodes; ++i) {
+    if (!nodes[i]) return set_error("null node"), NB_E_ARG;
+    if (i > 0 && (parent[i] < 0 || parent[i] >= i)) return set_error("parent[i] must precede i"), NB_E_ARG;
+    if (nodes[i]->device != nodes[0]->device || nodes[i]->d0 != nodes[0]->d0)
+      return set_error("nodes must share the device and the record layout"), NB_E_ARG;
+    if (nodes[i]->comm) return set_error("hierarchies run on one GPU"), NB_E_UNSUPPORTED;
+  }
+  DeviceGuard g(nodes[0]->device);
+  unsigned long long c[4] = {0, 0, 0, 0};
+  NB_CUDA(hier_score(nodes, n_nodes, parent, q, y, n, c, (cudaStream_t)stream, hier_forward));
+  memset(out, 0, sizeof(*out));
+  out->tp = c[0]; out->fp = c[1]; out->fn = c[2]; out->tn = c[3];
+  return NB_OK;
+}
+
 nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uint8_t* host,
                          int32_t device, nb_grid** out) {
   if (!host || !out || space_dim < 2 || space_dim > 4 || R < 1 || R > 4096 ||

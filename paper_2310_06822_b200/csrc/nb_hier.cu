@@ -1,0 +1,142 @@
+// nb_hier.cu — neural bounding hierarchies (P:224-229
+// §3.2: "stack our neural bounding volumes into hierarchies ... the tree's
+// structure needs to be supplied by the user").
+//
+// Every node is an nb_model bounding the union of the indicators below it;
+// a query is predicted positive iff some root-to-leaf path has every node
+// predicting positive (each node's own calibrated predictor, exit heads
+// included).  Evaluation prunes like a BVH: a node runs only on the rows its
+// parent passed — the rows are gathered into a dense array, scored by the
+// node's fused forward kernel, and the passing rows compacted into the
+// node's survivor list; leaves mark their survivors.  Per-node row order is
+// not fixed (warp-aggregated compaction), but each row's logits are computed
+// independently, so the predicted set and the counts are exact.
+#include <algorithm>
+#include <vector>
+
+#include "nb_device.cuh"
+#include "nb_internal.cuh"
+
+namespace nb {
+
+namespace {
+
+__global__ void k_gather(const float* __restrict__ q, const int32_t* __restrict__ idx, int64_t c, int d0,
+                         float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c * d0;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d0;
+    out[e] = q[(int64_t)idx[r] * d0 + e % d0];
+  }
+}
+
+// rows of this node whose predictor passes: yhat = [e_1 >= tau_1][e_2 >= tau_2][z >= tau]
+__global__ void k_compact(const float* __restrict__ logits, int nl, float t0, float t1, float t2,
+                          const int32_t* __restrict__ idx_in, int64_t c, int32_t* __restrict__ idx_out,
+                          unsigned long long* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < c;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = base + lane;
+    bool pass = false;
+    if (r < c) {
+      const float* z = logits + r * nl;
+      pass = z[0] >= t0 && (nl < 2 || z[1] >= t1) && (nl < 3 || z[2] >= t2);
+    }
+    const uint32_t b = __ballot_sync(0xFFFFFFFFu, pass);
+    unsigned long long off = 0;
+    if (lane == 0 && b) off = atomicAdd(count, (unsigned long long)__popc(b));
+    off = __shfl_sync(0xFFFFFFFFu, off, 0);
+    if (pass) idx_out[off + __popc(b & ((1u << lane) - 1u))] = idx_in ? idx_in[r] : (int32_t)r;
+  }
+}
+
+__global__ void k_mark(const int32_t* __restrict__ idx, int64_t c, uint8_t* __restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < c; r += (int64_t)gridDim.x * blockDim.x)
+    flag[idx[r]] = 1;
+}
+
+__global__ void k_hier_count(const uint8_t* __restrict__ flag, const uint8_t* __restrict__ y, int64_t n,
+                             unsigned long long* __restrict__ counts) {
+  uint32_t c[4] = {0, 0, 0, 0};
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = base + lane;
+    const bool v = r < n, p = v && flag[r], yy = v && y[r];
+    c[0] += __popc(__ballot_sync(0xFFFFFFFFu, p && yy));
+    c[1] += __popc(__ballot_sync(0xFFFFFFFFu, p && !yy));
+    c[2] += __popc(__ballot_sync(0xFFFFFFFFu, v && !p && yy));
+    c[3] += __popc(__ballot_sync(0xFFFFFFFFu, v && !p && !yy));
+  }
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k)
+      if (c[k]) atomicAdd(counts + k, (unsigned long long)c[k]);
+}
+
+unsigned grid_for(int64_t work) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8)); }
+
+}  // namespace
+
+cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* parent, const float* q,
+                       const uint8_t* y, int64_t n, unsigned long long* h_counts, cudaStream_t st,
+                       cudaError_t (*forward)(const nb_model*, const float*, int64_t, float*, cudaStream_t)) {
+  const nb_model* root = nodes[0];
+  const int d0 = root->d0;
+  int nlmax = 1;
+  for (int i = 0; i < n_nodes; ++i) nlmax = std::max(nlmax, 1 + nodes[i]->d.n_heads);
+  // scratch: survivor lists per node, gathered records, logits, flags, counters
+  // (every sub-buffer 256-B aligned: the node kernels bulk-copy records with TMA)
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t idx_bytes = up(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
+  const size_t q_bytes = up(sizeof(float) * (size_t)n * d0), l_bytes = up(sizeof(float) * (size_t)n * nlmax);
+  const size_t f_bytes = up((size_t)n + 1);
+  const size_t bytes = idx_bytes * n_nodes + q_bytes + l_bytes + f_bytes + up(8 * (4 + (size_t)n_nodes));
+  uint8_t* base = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&base, bytes, st);
+  if (e != cudaSuccess) return e;
+  int32_t* idx = (int32_t*)base;
+  float* qg = (float*)(base + idx_bytes * n_nodes);
+  float* lg = (float*)((uint8_t*)qg + q_bytes);
+  uint8_t* flag = (uint8_t*)lg + l_bytes;
+  unsigned long long* cnt = (unsigned long long*)(flag + f_bytes);
+  unsigned long long* node_cnt = cnt + 4;  // survivors per node
+  e = cudaMemsetAsync(flag, 0, (size_t)n, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (4 + n_nodes), st);
+  std::vector<unsigned long long> surv(n_nodes, 0);
+  std::vector<char> is_leaf(n_nodes, 1);
+  for (int i = 1; i < n_nodes; ++i) is_leaf[parent[i]] = 0;
+  for (int i = 0; i < n_nodes && e == cudaSuccess; ++i) {
+    const nb_model* m = nodes[i];
+    const int nl = 1 + m->d.n_heads;
+    const int32_t* in = i == 0 ? nullptr : idx + (size_t)parent[i] * (idx_bytes / 4);
+    const int64_t c = i == 0 ? n : (int64_t)surv[parent[i]];
+    int32_t* out = idx + (size_t)i * (idx_bytes / 4);
+    if (c > 0) {
+      const float* src = q;
+      if (i > 0) {
+        k_gather<<<grid_for(c * d0), 256, 0, st>>>(q, in, c, d0, qg);
+        src = qg;
+      }
+      e = forward(m, src, c, lg, st);
+      if (e != cudaSuccess) break;
+      k_compact<<<grid_for(c), 256, 0, st>>>(lg, nl, m->tau[0], m->tau[1], m->tau[2], in, c, out, node_cnt + i);
+      if (is_leaf[i]) {
+        e = cudaMemcpyAsync(&surv[i], node_cnt + i, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess && surv[i] > 0) k_mark<<<grid_for((int64_t)surv[i]), 256, 0, st>>>(out, (int64_t)surv[i], flag);
+      } else {
+        e = cudaMemcpyAsync(&surv[i], node_cnt + i, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      }
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && n > 0) k_hier_count<<<grid_for(n), 256, 0, st>>>(flag, y, n, cnt);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_counts, cnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(base, st);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace nb
