@@ -94,3 +94,41 @@ def test_gpu_hierarchy_matches_oracle_and_is_conservative():
     # the hierarchy prunes: it never predicts more than the root alone
     assert c["tp"] + c["fp"] <= models[0].score(qd, torch.from_numpy(ys[0]).cuda())["tp"] + \
         models[0].score(qd, torch.from_numpy(ys[0]).cuda())["fp"]
+
+
+@pytest.mark.gpu
+def test_gpu_hierarchy_argument_checks_and_fp32_nodes():
+    """Malformed trees are rejected; fp32 (CUDA-core) node models take the
+    same path (forward -> compaction) and agree with the oracle exactly."""
+    import paper_2310_06822_b200 as nb
+    from gpu_helpers import grid_of
+    cfg = nbgen.CONFIGS["c1"]
+    grid = grid_of(cfg)
+    n = 20000
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = oracle.label(grid, 2, "point", q.numpy())
+    qd, yd = q.cuda(), torch.from_numpy(y).cuda()
+    a = oracle.make_arch(2, 32, 2)
+    models, thetas, taus = [], [], []
+    for i in range(3):
+        th = torch.from_numpy(np.random.default_rng(10 + i).normal(size=oracle.num_params(a)) * 0.6).float()
+        m = nb.Model(nb.Desc("point", 2, 32, 2, (), "fp32"), 0)
+        m.set_params(th)
+        m.set_thresholds([0.1 * i - 0.05])
+        models.append(m)
+        thetas.append(th.double().numpy())
+        taus.append(np.array([0.1 * i - 0.05]))
+    for bad in ([0, 0, 0], [-1, 2, 0], [-1, 0, 5]):
+        with pytest.raises(nb.NBError):
+            nb.hier_score(models, bad, qd, yd)
+    parent = [-1, 0, 0]
+    c = nb.hier_score(models, parent, qd, yd)
+    z = [oracle.forward(a, th, q.numpy())[:, 0] for th in thetas]
+    keep = np.all([np.abs(zi - t[0]) > 1e-4 for zi, t in zip(z, taus)], axis=0)
+    pred = oracle.hier_combine(parent, [zi >= np.float32(t[0]) for zi, t in zip(z, taus)])
+    sub = nb.hier_score(models, parent, qd[torch.from_numpy(keep).cuda()], yd[torch.from_numpy(keep).cuda()])
+    yy = y[keep].astype(bool)
+    p = pred[keep]
+    assert (sub["tp"], sub["fp"], sub["fn"], sub["tn"]) == (int((p & yy).sum()), int((p & ~yy).sum()),
+                                                            int((~p & yy).sum()), int((~p & ~yy).sum()))
+    assert c["tp"] + c["fp"] + c["fn"] + c["tn"] == n

@@ -25,6 +25,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 logn = int(sys.argv[2]) if len(sys.argv) > 2 else 22
 cfg = nbgen.CONFIGS[name]
 n = 1 << logn
+if len(sys.argv) > 3:  # explicit row count (e.g. an exact multiple of 148 CTAs x slots x 128)
+    n = int(sys.argv[3])
 q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n, device="cuda")
 g = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, 0)
 y = g.label(cfg.kind, q)
