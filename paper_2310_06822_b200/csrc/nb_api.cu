@@ -815,10 +815,13 @@ nb_status nb_comm_version(int32_t* v) {
   return NB_OK;
 }
 
-// Node forward for the hierarchy: the model's fused kernel in forward mode.
-static cudaError_t hier_forward(const nb_model* m, const float* q, int64_t n, float* logits, cudaStream_t s) {
+// Node forward for the hierarchy: the model's fused kernel in forward mode,
+// its row count read on the device (n_dev) below the launch's upper bound n.
+static cudaError_t hier_forward(const nb_model* m, const float* q, int64_t n, const unsigned long long* n_dev,
+                                float* logits, cudaStream_t s) {
   FwdArgs a = base_args(m, q, nullptr, n);
   a.logits = logits;
+  a.n_dev = n_dev;
   return launch_forward_any(m, kForward, a, s);
 }
 
@@ -833,6 +836,9 @@ nb_status nb_hier_score(nb_model* const* nodes, int32_t n_nodes, const int32_t* 
     if (nodes[i]->device != nodes[0]->device || nodes[i]->d0 != nodes[0]->d0)
       return set_error("nodes must share the device and the record layout"), NB_E_ARG;
     if (nodes[i]->comm) return set_error("hierarchies run on one GPU"), NB_E_UNSUPPORTED;
+    // node kernels read their row count on the device (k_fwd_tc, k_fwd_simt)
+    if (nodes[i]->pl.pairs != 1)
+      return set_error("hierarchy nodes: widths <= 128 (no CTA-pair models)"), NB_E_UNSUPPORTED;
   }
   DeviceGuard g(nodes[0]->device);
   unsigned long long c[4] = {0, 0, 0, 0};

@@ -358,7 +358,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   }
   mbar_wait(smem_u32(bars), 0);
 
-  const int64_t n = p.a.n;
+  const bool dyn_n = MODE == kForward && p.a.n_dev;  // device-side row count (hierarchies)
+  const int64_t n = dyn_n ? (int64_t)*p.a.n_dev : p.a.n;
+  const int64_t num_tiles = dyn_n ? (n + kTile - 1) / kTile : p.num_tiles;
   const int64_t G = gridDim.x;
 
   const int s = warp / WPS;              // tile slot
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   // read directly.
   auto full_tile = [&](int64_t t) { return (t + 1) * kTile <= n; };
   auto stage_issue = [&](int64_t t, int b) {
-    if (!issuer || t >= p.num_tiles || !full_tile(t)) return;
+    if (!issuer || t >= num_tiles || !full_tile(t)) return;
     const uint32_t qb = (uint32_t)(kTile * d0 * 4);
     const uint32_t bar = stage_bar(s, b);
     constexpr bool kY = MODE != kForward;
@@ -488,9 +490,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   stage_issue(tile, 0);
   stage_issue(tile + NSLOT * G, 1);
   int i_tile = 0;
-  if (tile < p.num_tiles) put_input(tile, 0);
+  if (tile < num_tiles) put_input(tile, 0);
   uint32_t par = 0;
-  while (tile < p.num_tiles) {
+  while (tile < num_tiles) {
     const int64_t next = tile + NSLOT * G;
     int ythis = 0;
     float z0 = lead ? bout : 0.f, z1 = 0.f;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         // the slot's next tile now so its layer-0 MMA overlaps this epilogue
         ythis = ycur;
         ++i_tile;
-        if (next < p.num_tiles) put_input(next, i_tile);
+        if (next < num_tiles) put_input(next, i_tile);
       }
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     if (!kAllLoads) {
       ythis = ycur;
       ++i_tile;
-      if (next < p.num_tiles) put_input(next, i_tile);
+      if (next < num_tiles) put_input(next, i_tile);
     }
     float z = z0 + z1;
     float e[2] = {e0a + e0b, e1a + e1b};

@@ -21,8 +21,9 @@ namespace nb {
 
 namespace {
 
-__global__ void k_gather(const float* __restrict__ q, const int32_t* __restrict__ idx, int64_t c, int d0,
-                         float* __restrict__ out) {
+__global__ void k_gather(const float* __restrict__ q, const int32_t* __restrict__ idx,
+                         const unsigned long long* __restrict__ c_dev, int d0, float* __restrict__ out) {
+  const int64_t c = (int64_t)*c_dev;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < c * d0;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / d0;
@@ -31,9 +32,11 @@ __global__ void k_gather(const float* __restrict__ q, const int32_t* __restrict_
 }
 
 // rows of this node whose predictor passes: yhat = [e_1 >= tau_1][e_2 >= tau_2][z >= tau]
+// (c_dev: row count written by the previous node's compaction; NULL -> c)
 __global__ void k_compact(const float* __restrict__ logits, int nl, float t0, float t1, float t2,
-                          const int32_t* __restrict__ idx_in, int64_t c, int32_t* __restrict__ idx_out,
-                          unsigned long long* __restrict__ count) {
+                          const int32_t* __restrict__ idx_in, int64_t c, const unsigned long long* __restrict__ c_dev,
+                          int32_t* __restrict__ idx_out, unsigned long long* __restrict__ count) {
+  if (c_dev) c = (int64_t)*c_dev;
   const int lane = threadIdx.x & 31;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < c;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -51,7 +54,9 @@ __global__ void k_compact(const float* __restrict__ logits, int nl, float t0, fl
   }
 }
 
-__global__ void k_mark(const int32_t* __restrict__ idx, int64_t c, uint8_t* __restrict__ flag) {
+__global__ void k_mark(const int32_t* __restrict__ idx, const unsigned long long* __restrict__ c_dev,
+                       uint8_t* __restrict__ flag) {
+  const int64_t c = (int64_t)*c_dev;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < c; r += (int64_t)gridDim.x * blockDim.x)
     flag[idx[r]] = 1;
 }
@@ -78,15 +83,19 @@ unsigned grid_for(int64_t work) { return (unsigned)std::max<int64_t>(1, std::min
 
 }  // namespace
 
+// Every launch is sized for the upper bound n (survivor counts never leave
+// the device: the node kernels read their row count from the previous
+// node's compaction counter), so the whole tree is enqueued without a host
+// round trip; forward(m, q, n_upper, n_dev, logits, st) is the node's fused
+// forward reading its row count from n_dev (NULL: n_upper rows).
 cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* parent, const float* q,
                        const uint8_t* y, int64_t n, unsigned long long* h_counts, cudaStream_t st,
-                       cudaError_t (*forward)(const nb_model*, const float*, int64_t, float*, cudaStream_t)) {
-  const nb_model* root = nodes[0];
-  const int d0 = root->d0;
+                       cudaError_t (*forward)(const nb_model*, const float*, int64_t,
+                                              const unsigned long long*, float*, cudaStream_t)) {
+  const int d0 = nodes[0]->d0;
   int nlmax = 1;
   for (int i = 0; i < n_nodes; ++i) nlmax = std::max(nlmax, 1 + nodes[i]->d.n_heads);
-  // scratch: survivor lists per node, gathered records, logits, flags, counters
-  // (every sub-buffer 256-B aligned: the node kernels bulk-copy records with TMA)
+  // scratch (every sub-buffer 256-B aligned: the node kernels bulk-copy records with TMA)
   auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t idx_bytes = up(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
   const size_t q_bytes = up(sizeof(float) * (size_t)n * d0), l_bytes = up(sizeof(float) * (size_t)n * nlmax);
@@ -103,34 +112,28 @@ cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* paren
   unsigned long long* node_cnt = cnt + 4;  // survivors per node
   e = cudaMemsetAsync(flag, 0, (size_t)n, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (4 + n_nodes), st);
-  std::vector<unsigned long long> surv(n_nodes, 0);
   std::vector<char> is_leaf(n_nodes, 1);
   for (int i = 1; i < n_nodes; ++i) is_leaf[parent[i]] = 0;
-  for (int i = 0; i < n_nodes && e == cudaSuccess; ++i) {
+  for (int i = 0; i < n_nodes && e == cudaSuccess && n > 0; ++i) {
     const nb_model* m = nodes[i];
     const int nl = 1 + m->d.n_heads;
-    const int32_t* in = i == 0 ? nullptr : idx + (size_t)parent[i] * (idx_bytes / 4);
-    const int64_t c = i == 0 ? n : (int64_t)surv[parent[i]];
     int32_t* out = idx + (size_t)i * (idx_bytes / 4);
-    if (c > 0) {
-      const float* src = q;
-      if (i > 0) {
-        k_gather<<<grid_for(c * d0), 256, 0, st>>>(q, in, c, d0, qg);
-        src = qg;
-      }
-      e = forward(m, src, c, lg, st);
+    if (i == 0) {
+      e = forward(m, q, n, nullptr, lg, st);
       if (e != cudaSuccess) break;
-      k_compact<<<grid_for(c), 256, 0, st>>>(lg, nl, m->tau[0], m->tau[1], m->tau[2], in, c, out, node_cnt + i);
-      if (is_leaf[i]) {
-        e = cudaMemcpyAsync(&surv[i], node_cnt + i, 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess && surv[i] > 0) k_mark<<<grid_for((int64_t)surv[i]), 256, 0, st>>>(out, (int64_t)surv[i], flag);
-      } else {
-        e = cudaMemcpyAsync(&surv[i], node_cnt + i, 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      }
+      k_compact<<<grid_for(n), 256, 0, st>>>(lg, nl, m->tau[0], m->tau[1], m->tau[2], nullptr, n, nullptr, out,
+                                            node_cnt);
+    } else {
+      const int32_t* in = idx + (size_t)parent[i] * (idx_bytes / 4);
+      const unsigned long long* c_in = node_cnt + parent[i];
+      k_gather<<<grid_for(n * d0), 256, 0, st>>>(q, in, c_in, d0, qg);
+      e = forward(m, qg, n, c_in, lg, st);
+      if (e != cudaSuccess) break;
+      k_compact<<<grid_for(n), 256, 0, st>>>(lg, nl, m->tau[0], m->tau[1], m->tau[2], in, 0, c_in, out,
+                                            node_cnt + i);
     }
-    if (e == cudaSuccess) e = cudaGetLastError();
+    if (is_leaf[i]) k_mark<<<grid_for(n), 256, 0, st>>>(out, node_cnt + i, flag);
+    e = cudaGetLastError();
   }
   if (e == cudaSuccess && n > 0) k_hier_count<<<grid_for(n), 256, 0, st>>>(flag, y, n, cnt);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h_counts, cnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st);

@@ -177,6 +177,9 @@ struct FwdArgs {
   unsigned int* keys;
   unsigned int* flags;
   int invert;  // kCalibrate: certainly-hit threshold (min of -z over negatives, nb_calibrate_inverted)
+  // kForward of k_fwd_tc: when set, the row count is read from device memory
+  // (written by an earlier kernel; n is then only the launch's upper bound)
+  const unsigned long long* n_dev;
   TrainArgs tr;
 };
 
@@ -211,7 +214,8 @@ cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_sat2_build(nb_grid* g, cudaStream_t s);
 cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* parent, const float* q,
                        const uint8_t* y, int64_t n, unsigned long long* h_counts, cudaStream_t st,
-                       cudaError_t (*forward)(const nb_model*, const float*, int64_t, float*, cudaStream_t));
+                       cudaError_t (*forward)(const nb_model*, const float*, int64_t,
+                                              const unsigned long long*, float*, cudaStream_t));
 
 // NCCL (dlopen'ed); all return 0 on success
 int comm_unique_id(uint8_t id[128]);

@@ -237,10 +237,11 @@ __global__ void __launch_bounds__(256) k_fwd_simt(const float* __restrict__ thet
   acc.init();
   const int nl = 1 + s.nh;
   const int64_t warp_stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < a.n;
+  const int64_t n = (MODE == kForward && a.n_dev) ? (int64_t)*a.n_dev : a.n;  // hierarchies
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
        base += warp_stride) {
     const int64_t i = base + (threadIdx.x & 31);
-    const bool valid = i < a.n;
+    const bool valid = i < n;
     float h[W];
     float e[2] = {0.f, 0.f};
     bool bad = false;
