@@ -48,3 +48,18 @@ def test_invalid_desc_rejected_without_gpu():
     assert nb.lib().nb_num_params(C.byref(d)) == -1
     h = C.c_void_p()
     assert nb.lib().nb_model_create(C.byref(d), 0, C.byref(h)) == 1  # NB_E_ARG
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/nb.h is a C ABI: it compiles as strict C99 (no C++ or torch types)."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    src = tmp_path / "use.c"
+    src.write_text('#include "nb.h"\nint main(void) { nb_desc d = {0}; nb_counts c; nb_schedule s;\n'
+                   '  (void)d; (void)c; (void)s; return nb_record_floats(NB_POINT, 3) == 3 ? 0 : 1; }\n')
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                        os.path.join(ROOT, "include"), "-c", str(src), "-o", str(tmp_path / "use.o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
