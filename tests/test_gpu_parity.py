@@ -943,3 +943,23 @@ def test_gpu_2d_labellers_bit_exact_and_kernels(kind):
     cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
     co = oracle.score(ze[keep], y[keep], te)
     assert all(cg[k] == co[k] for k in ("tp", "fp", "fn", "tn")), (cg, co)
+
+
+@pytest.mark.parametrize("width,pe", [(64, 0), (128, 8)])
+def test_sine_pe_train_micro_batches_equal_one_batch(width, pe, monkeypatch):
+    """Sine / PE training split into micro-batches (the cos images and the
+    K = 64 layer-1 image per chunk) gives the single-batch gradient up to
+    fp32 summation order."""
+    cfg, desc, a, q, y, th = _sine_case("c1", width, 3, pe, "bf16", 5 * 1024 + 77, seed=4)
+    out = []
+    for chunk in (None, "1024"):
+        if chunk:
+            monkeypatch.setenv("NB_TRAIN_CHUNK", chunk)
+        m = nb.Model(desc, DEV)
+        m.set_params(torch.from_numpy(th).float())
+        st = m.train_step(cuda(q), cuda(y), alpha=20.0, beta=1.0, lr=1e-3, stats=True)
+        out.append((st, m.get_grad().double().numpy()))
+        monkeypatch.delenv("NB_TRAIN_CHUNK", raising=False)
+    (s1, g1), (s2, g2) = out
+    assert all(s1[k] == s2[k] for k in ("tp", "fp", "fn", "tn"))
+    assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g1)
