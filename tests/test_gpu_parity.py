@@ -963,3 +963,33 @@ def test_sine_pe_train_micro_batches_equal_one_batch(width, pe, monkeypatch):
     (s1, g1), (s2, g2) = out
     assert all(s1[k] == s2[k] for k in ("tp", "fp", "fn", "tn"))
     assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g1)
+
+
+def test_bf16_sine_with_exit_heads():
+    """Sine nets with early-exit heads (heads read sin(z_l), R41/R22) take the
+    dense EXT kernels (compaction is ReLU-only): every head's logit within the
+    bf16 tolerance of fp64, counts and exit histogram equal to the
+    bf16-emulating oracle outside the band."""
+    cfg = nbgen.CONFIGS["c4"]
+    n = (1 << 14) + 9
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    a = oracle.make_arch(4, 128, 6, (2, 4), act="sine")
+    th = np.random.default_rng(6).uniform(-1, 1, oracle.num_params(a)) * 0.9 * np.sqrt(6.0 / 256)
+    m = nb.Model(nb.Desc("point", 4, 128, 6, (2, 4), "bf16", activation="sine"), DEV)
+    m.set_params(torch.from_numpy(th).float())
+    th32 = torch.from_numpy(th).float().double().numpy()
+    qd, yd = cuda(q), cuda(y)
+    zg = m.forward(qd).cpu().double().numpy()
+    zr = oracle.forward(a, th32, q.numpy())
+    assert np.max(np.abs(1 / (1 + np.exp(-zg)) - 1 / (1 + np.exp(-zr)))) <= 2e-2
+    tau = m.calibrate(qd, yd).numpy()
+    assert m.score(qd, yd)["fn"] == 0
+    ze = oracle.forward(a, th32, q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    keep = ~band_mask(zg, tau, ze, te)
+    assert keep.mean() > 0.9
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    for k in ("tp", "fp", "fn", "tn", "exit_hist"):
+        assert cg[k] == co[k], (k, cg, co)
