@@ -4,16 +4,21 @@
 
 A step is one pass of the fused hot path (encode -> MLP on tcgen05 -> classify
 with the calibrated threshold -> FP/FN/TP/TN counts -> NCCL allreduce of the
-counts across ranks) over one batch of BASELINE.json configs[1] ("c2": 3D
-point bounding, 3 -> 64x4 -> 1 bf16, 2^22 uniform points per forward pass).
-Inputs are seeded synthetic (nbgen), labels come from the library's GPU
-labeller, thresholds from nb_calibrate; the timed region is nb_score_async
-(kernel + count allreduce + the step's count readback into pinned memory).
+counts across ranks) over one batch of the workload BASELINE.json's metric
+("bounding queries/s (1/2/4/8 B200)") is quoted on: configs[4] ("c5": 3D box
+bounding, 6 -> 256x4 -> 1 bf16, "2^28 box queries sharded over 1/2/4/8
+GPUs").  Inputs are seeded synthetic (nbgen), labels come from the library's
+GPU labeller, the model is trained through nb_train_step and calibrated with
+nb_calibrate; the timed region is nb_score_async (kernel + count allreduce +
+the step's count readback into pinned memory).
 
-Weak scaling: every rank scores its own 2^22-query shard (rows r*2^22.. of the
-EVAL stream); value = all ranks' queries / max-over-ranks device time.
-L2 (126 MB) is flushed by writing a 256 MiB buffer between timed steps (the
-step's inputs are 52 MB), outside the timed events.
+Strong scaling (c5): the 2^28 queries of a step are split into tile-aligned
+contiguous shards (dist.shard), one per rank; value = 2^28 x steps / the
+max-over-ranks device time.  --config c2|c3|c4 time the other BASELINE
+configs (weak scaling: each rank its own full batch).  --gpus N without
+torchrun re-launches this script under torch.distributed.run with N ranks.
+L2 (126 MB) is flushed by writing a 256 MiB buffer between timed steps,
+outside the timed events.
 
 --impl reference times the oracle (oracle/, plain C fp64) on the host cores on
 a bounded sample of the same workload; under torchrun only rank
@@ -32,7 +37,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = "c2"  # --config: c2 (default, BASELINE.json configs[1]) .. c5
+CONFIG = "c5"  # --config: c5 (default: the metric's "1/2/4/8 B200" workload, BASELINE.json configs[4]) or c2..c4
 # Queries per step (BASELINE.json): c2 2^22, c3 2^24, c4 2^26 per rank (weak
 # scaling); c5 2^28 in total, sharded over the ranks (strong scaling, BJ.c5).
 N_STEP = {"c2": 1 << 22, "c3": 1 << 24, "c4": 1 << 26, "c5": 1 << 28}
@@ -52,6 +57,9 @@ KERNEL = {"c2": "k_fwd_tc<64,4,0,0,kScore,d0=3,BF>", "c3": "k_fwd_tc<128,4,0,0,k
           "c5": "k_fwd_tc2<4,kScore,BF> (CTA pairs)"}
 METRIC = "bounding queries/s"
 UNIT = "queries/s"
+# bounded oracle samples (about 10 s of host work per step at 16 cores)
+CPU_SAMPLE = {"c2": 1 << 23, "c3": 1 << 21, "c4": 1 << 21, "c5": 1 << 20}
+REF_SAMPLE = {"c2": 1 << 20, "c3": 1 << 18, "c4": 1 << 18, "c5": 1 << 17}
 
 
 def flop_per_query(cfg) -> int:
@@ -77,10 +85,12 @@ def executed_flop_per_query(cfg, hist, n) -> float:
     return 2 * (f0 + s1 * f1 + s2 * f2)
 
 
-def train_for_exits(nb, nbgen, m, grid, cfg, steps, rank, world):
-    """c4's exit heads only skip work once trained: the bench model is trained
-    for `steps` Adam steps with Eq. (1) on fresh TRAIN batches (the config's
-    batch split over the ranks, alpha ramp 1 -> 1000) before calibration."""
+def train_model(nb, nbgen, m, grid, cfg, steps, rank, world):
+    """The bench scores a trained bounding model (c4's exit heads only skip
+    work once trained): `steps` Adam steps of Eq. (1) through nb_train_step
+    on fresh TRAIN batches (the config's global batch split over the ranks,
+    gradient allreduce under a communicator, alpha ramp 1 -> 1000), then
+    calibration."""
     dev = f"cuda:{m.device}"
     B = cfg.train_batch
     for t in range(steps):
@@ -193,7 +203,7 @@ def run_reference(args):
     a = oracle.arch_of(cfg)
     grid = nbgen.make_grid(cfg).numpy()
     th = (nbgen.init_params(cfg) * 2.5).double().numpy()
-    n = args.ref_sample
+    n = args.ref_sample or REF_SAMPLE[CONFIG]
     q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n).numpy()
     frames = grid.shape[0] if cfg.space_dim == 4 else 1
     y = oracle.label(grid, cfg.space_dim, cfg.kind, q, frames=frames)
@@ -212,7 +222,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if CONFIG in STRONG else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{CONFIG}: {WORKLOAD[CONFIG]}; oracle sample of {n} queries per step",
                    "global_batch": n},
@@ -266,16 +277,18 @@ def run_ours(args):
         from paper_2310_06822_b200.dist import comm_init
 
         comm_init(m)
+    from paper_2310_06822_b200.dist import shard
+
     strong = CONFIG in STRONG
-    n = N_STEP[CONFIG] // world if strong else N_STEP[CONFIG]
+    if strong:   # the step's 2^28 queries, tile-aligned contiguous shards
+        s0, n = shard(N_STEP[CONFIG], rank, world)
+    else:        # weak scaling: every rank its own full batch
+        s0, n = rank * N_STEP[CONFIG], N_STEP[CONFIG]
     grid = nb.Grid(nbgen.make_grid(cfg), cfg.space_dim, local)
-    exits = cfg.n_heads > 0 and args.exit_train_steps > 0
-    if exits:
-        m.set_params(nbgen.init_params(cfg))
-        train_for_exits(nb, nbgen, m, grid, cfg, args.exit_train_steps, rank, world)
-    else:
-        m.set_params(nbgen.init_params(cfg) * 2.5)
-    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, rank * n, n, device=dev)
+    m.set_params(nbgen.init_params(cfg))
+    if args.model_train_steps > 0:
+        train_model(nb, nbgen, m, grid, cfg, args.model_train_steps, rank, world)
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, s0, n, device=dev)
     y = grid.label(cfg.kind, q)
     tau = m.calibrate(q, y)                       # global tau (allreduce min across ranks)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > the 126 MB L2
@@ -320,7 +333,8 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, kernel_ms = t.tolist()
-    total_q = n * world * args.steps
+    n_total = N_STEP[CONFIG] if strong else n * world
+    total_q = n_total * args.steps
     value = total_q / (dev_ms * 1e-3)
     # ---------------- roofline of the dominant kernel ----------------
     fq = flop_per_query(cfg)
@@ -329,7 +343,7 @@ def run_ours(args):
     per_launch_ms = kernel_ms / max(1, calls)
     exit_info = None
     if cfg.n_heads > 0:
-        fq_exec = executed_flop_per_query(cfg, c["exit_hist"], n)
+        fq_exec = executed_flop_per_query(cfg, c["exit_hist"], n_total)
         achieved = fq_exec * n / (per_launch_ms * 1e-3) / 1e12
         # the dense kernel (every head on every row) on the same model, same protocol
         nb.lib().nb_debug_set_dense_exits(1)
@@ -349,12 +363,12 @@ def run_ours(args):
         assert m.counts_dict(out[0]) == c
         dense_ms = sorted(dts)[len(dts) // 2]
         exit_info = {"exit_hist": c["exit_hist"], "bins": "exit@1, exit@2, final-negative, final-positive",
-                     "survive_head1": (n - c["exit_hist"][0]) / n,
-                     "survive_head2": (n - c["exit_hist"][0] - c["exit_hist"][1]) / n,
+                     "survive_head1": (n_total - c["exit_hist"][0]) / n_total,
+                     "survive_head2": (n_total - c["exit_hist"][0] - c["exit_hist"][1]) / n_total,
                      "executed_flop_per_query": fq_exec, "dense_flop_per_query": fq,
-                     "dense_kernel_q_per_s": n * world / (dense_ms * 1e-3),
+                     "dense_kernel_q_per_s": n_total / (dense_ms * 1e-3),
                      "dense_kernel_ms_per_step": dense_ms,
-                     "model": f"trained {args.exit_train_steps} Adam steps (Eq. 1, alpha 1->1000) "
+                     "model": f"trained {args.model_train_steps} Adam steps (Eq. 1, alpha 1->1000) "
                               "from Xavier init, calibrated to FN = 0 on the step's queries"}
     else:
         achieved = fq * n / (per_launch_ms * 1e-3) / 1e12
@@ -390,7 +404,9 @@ def run_ours(args):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {"workload": f"{CONFIG}: {WORKLOAD[CONFIG]}, fused forward+calibrated score+counts",
-                       "global_batch": n * world, "per_rank_batch": n,
+                       "global_batch": n_total, "per_rank_batch": n,
+                       "model": f"Xavier init + {args.model_train_steps} Adam steps of Eq. (1) "
+                                f"(batch {cfg.train_batch}, alpha 1->1000) via nb_train_step, then nb_calibrate",
                        "parallelism": f"dp{world} (query shards, NCCL allreduce of counts)",
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -400,7 +416,8 @@ def run_ours(args):
                          "kernel_ms_per_launch": per_launch_ms,
                          "ncu_tensor_pipe_pct": tensor_pct},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (4 * cfg.record_floats + 1),
-                    "d2h_bytes_per_step": 9 * 8, "api": "nb_score_host (pinned host q/y)"},
+                    "d2h_bytes_per_step": 9 * 8, "api": "nb_score_host (pinned host q/y)",
+                    "bytes": "per rank"},
             "gpu_launches": launches,
             "clocks": clocks,
             "counts": {k: c[k] for k in ("tp", "fp", "fn", "tn")},
@@ -411,7 +428,7 @@ def run_ours(args):
         if exit_info is not None:
             line["early_exit"] = exit_info
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_sample or CPU_SAMPLE[CONFIG])
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -464,25 +481,80 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
             "tflops_algorithmic": flop * B * steps / (ms * 1e-3) / 1e12}
 
 
+def free_port() -> int:
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn(args) -> int:
+    """--gpus N without torchrun: re-launch this script with N ranks under
+    torch.distributed.run (the driver's own launch line), one rank per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
+def run_dry(args):
+    """CPU rehearsal of the multi-rank launch (no GPU work): every rank joins a
+    gloo process group, computes its shard of the step, and rank 0 prints the
+    world it saw (tests/test_bench_contract.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_06822_b200.dist import shard
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    strong = CONFIG in STRONG
+    part = shard(N_STEP[CONFIG], rank, world) if strong else (rank * N_STEP[CONFIG], N_STEP[CONFIG])
+    t = torch.tensor([rank, world, part[0], part[1]], dtype=torch.int64)
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(parts, t)
+    else:
+        parts = [t]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": [int(p[0]) for p in parts],
+                          "shards": [[int(p[2]), int(p[3])] for p in parts], "config": CONFIG,
+                          "scaling": "strong" if strong else "weak"}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
-    ap.add_argument("--ref-sample", type=int, default=1 << 20)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 23)
+    ap.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--ref-sample", type=int, default=0, help="oracle rows per reference step (0: per config)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle rows of cpu_baseline (0: per config)")
     ap.add_argument("--train-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exit-train-steps", type=int, default=2000,
-                    help="c4: Adam steps before timing so the exit heads reject empty space")
+    ap.add_argument("--model-train-steps", type=int, default=2000,
+                    help="Adam steps on the bench model before calibration (c4: exit heads reject empty space)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU launch rehearsal (no GPU work)")
     args = ap.parse_args()
     global CONFIG
     CONFIG = args.config
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn(args))
+    if launched and args.impl == "ours" and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -18,6 +18,12 @@
  *      point: x (n floats; 4D is (x, y, z, t));  ray: (origin, unit direction);
  *      plane: (p0, unit normal);  box: (min corner, max corner).
  *  - Labels y are uint8 in {0, 1}, one per record.
+ *  - Alignment: device q and y passed to nb_forward, nb_calibrate*,
+ *    nb_score, nb_score_async, nb_train_step and nb_hier_score must be
+ *    16-byte aligned (the kernels stage whole 128-row tiles with
+ *    cp.async.bulk).  A misaligned pointer (e.g. a view starting at row 1)
+ *    returns NB_E_ARG before any launch.  Allocations are aligned; a row
+ *    offset r keeps both aligned when r is a multiple of 16.
  *  - The model owns its weights (fp32 master + packed bf16 copy), Adam state,
  *    thresholds, scratch and communicator; nothing is allocated on the hot path.
  *  - Calls filling host structs (nb_counts, tau_out, nb_step_stats) synchronise
@@ -263,8 +269,12 @@ nb_status nb_schedule_after_step(nb_schedule* s, uint64_t batch_fn);
  * predictor, exit heads included; R45).  Evaluated with pruning:
  * a node runs only on the rows its parent passed (gather -> the node's fused
  * forward -> compaction).  Writes tp/fp/fn/tn of that predictor against y
- * (exit_hist, nonfinite = 0).  All nodes on one device with the same record
- * layout, no communicator; n < 2^31.  Synchronises `stream` once per node.  */
+ * (exit_hist = 0) and in nonfinite the records with a non-finite logit at
+ * some evaluated node (they fail that node; warning-class NB_E_NONFINITE
+ * with the counts written).  All nodes on one device with the same record
+ * layout, no communicator; n < 2^31.  The whole tree is enqueued without
+ * host round trips and `stream` is synchronised once, at the end; scratch
+ * is held by nodes[0] and reused (it grows only when a call needs more).  */
 nb_status nb_hier_score(nb_model* const* nodes, int32_t n_nodes, const int32_t* parent, const float* q,
                         const uint8_t* y, int64_t n, nb_counts* out, void* stream);
 

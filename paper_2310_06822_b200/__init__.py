@@ -386,7 +386,7 @@ class Model:
         return None
 
 
-def hier_score(nodes, parent, q: torch.Tensor, y: torch.Tensor) -> dict:
+def hier_score(nodes, parent, q: torch.Tensor, y: torch.Tensor, allow_nonfinite: bool = False) -> dict:
     """Neural bounding hierarchy (nb_hier_score): counts of the
     predictor "some root-to-leaf path passes every node"."""
     dev = nodes[0].device
@@ -394,7 +394,8 @@ def hier_score(nodes, parent, q: torch.Tensor, y: torch.Tensor) -> dict:
     par = (C.c_int32 * len(parent))(*parent)
     c = _Counts()
     _check(lib().nb_hier_score(arr, len(nodes), par, nodes[0]._q(q), _dev_ptr(y, torch.uint8, dev, "y"),
-                               q.shape[0], C.byref(c), _stream(dev)), "nb_hier_score")
+                               q.shape[0], C.byref(c), _stream(dev)), "nb_hier_score",
+           (NB_OK, NB_E_NONFINITE) if allow_nonfinite else (NB_OK,))
     return c.as_dict()
 
 

@@ -211,6 +211,16 @@ struct DeviceGuard {
   }
 };
 
+// The fused kernels stage full 128-row tiles of q and y into shared memory
+// with cp.async.bulk, which needs 16-byte aligned global addresses (tile
+// offsets are multiples of 16 B, so the base pointers decide): misaligned
+// views are rejected before any launch (nb.h "Alignment").
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static nb_status misaligned(const char* where) {
+  set_error("%s: q and y must be 16-byte aligned device pointers", where);
+  return NB_E_ARG;
+}
+
 }  // namespace nb
 
 using namespace nb;
@@ -351,6 +361,7 @@ void nb_model_destroy(nb_model* m) {
   cudaFree(m->d_loss);
   cudaFree(m->train_scratch);
   cudaFree(m->exit_scratch);
+  cudaFree(m->hier_scratch);
   for (int i = 0; i < 2; ++i) {
     cudaFree(m->stage_q[i]);
     cudaFree(m->stage_y[i]);
@@ -498,6 +509,7 @@ nb_status nb_forward(const nb_model* m, const float* q, int64_t n, float* logits
                      void* stream) {
   if (!m || n < 0 || (n > 0 && (!q || !logits))) return set_error("bad argument"), NB_E_ARG;
   if (n == 0) return NB_OK;
+  if (!aligned16(q)) return misaligned("nb_forward");
   DeviceGuard g(m->device);
   FwdArgs a = base_args(m, q, nullptr, n);
   a.logits = logits;
@@ -511,6 +523,7 @@ static nb_status calibrate_impl(nb_model* m, const float* q, const uint8_t* y, i
   if (!m || !tau_out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
   if (invert && m->d.n_heads > 0)
     return set_error("inverted calibration: models without exit heads"), NB_E_UNSUPPORTED;
+  if (n > 0 && (!aligned16(q) || !aligned16(y))) return misaligned("nb_calibrate");
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = 1 + m->d.n_heads;
@@ -576,6 +589,7 @@ nb_status nb_score(const nb_model* m_, const float* q, const uint8_t* y, int64_t
                    void* stream) {
   nb_model* m = const_cast<nb_model*>(m_);
   if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  if (n > 0 && (!aligned16(q) || !aligned16(y))) return misaligned("nb_score");
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* fin = m->d_counts + kFinOff;
@@ -618,6 +632,7 @@ nb_status nb_score_async(const nb_model* m_, const float* q, const uint8_t* y, i
   static_assert(sizeof(nb_counts) == sizeof(unsigned long long) * kNumCounters, "nb_counts layout");
   nb_model* m = const_cast<nb_model*>(m_);
   if (!m || !out || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
+  if (n > 0 && (!aligned16(q) || !aligned16(y))) return misaligned("nb_score_async");
   DeviceGuard g(m->device);
   void* dout = device_view(out);
   if (!dout) return set_error("nb_score_async: out must be device or pinned host memory"), NB_E_ARG;
@@ -700,6 +715,7 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
       (n_local > 0 && (!q || !y)))
     return set_error("bad argument"), NB_E_ARG;
   if (!(alpha > 0.f) || !(beta >= 0.f) || !(lr > 0.f)) return set_error("bad alpha/beta/lr"), NB_E_ARG;
+  if (n_local > 0 && (!aligned16(q) || !aligned16(y))) return misaligned("nb_train_step");
   DeviceGuard g(m->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = m->d.precision == NB_BF16;
@@ -840,11 +856,17 @@ nb_status nb_hier_score(nb_model* const* nodes, int32_t n_nodes, const int32_t* 
     if (nodes[i]->pl.pairs != 1)
       return set_error("hierarchy nodes: widths <= 128 (no CTA-pair models)"), NB_E_UNSUPPORTED;
   }
+  if (!aligned16(q)) return misaligned("nb_hier_score");
   DeviceGuard g(nodes[0]->device);
-  unsigned long long c[4] = {0, 0, 0, 0};
+  unsigned long long c[5] = {0, 0, 0, 0, 0};
   NB_CUDA(hier_score(nodes, n_nodes, parent, q, y, n, c, (cudaStream_t)stream, hier_forward));
   memset(out, 0, sizeof(*out));
   out->tp = c[0]; out->fp = c[1]; out->fn = c[2]; out->tn = c[3];
+  out->nonfinite = c[4];
+  if (out->nonfinite) {  // warning-class, as nb_score: the counts are written
+    set_error("%llu records produced a non-finite logit", (unsigned long long)out->nonfinite);
+    return NB_E_NONFINITE;
+  }
   return NB_OK;
 }
 

@@ -72,7 +72,8 @@ int check(int r, const char* what) {
 
 int allreduce(nb_model* m, void* buf, size_t count, int dtype, int op, cudaStream_t s) {
   if (!m->comm) return 0;
-  if (m->world == 1) return 0;  // single-rank communicator: identity
+  // A one-rank communicator still runs the collective (a legal NCCL call), so
+  // the data-parallel path executes identically at every world size.
   return check(g_api.AllReduce(buf, buf, count, dtype, op, (Comm)m->comm, s), "ncclAllReduce");
 }
 }  // namespace

@@ -110,6 +110,9 @@ struct nb_model {
   // early-exit compaction scratch (nb_fwd_exit.cu): 2 image/label region sets
   void* exit_scratch = nullptr;
   size_t exit_scratch_bytes = 0;
+  // hierarchy scratch (nb_hier_score, held by the root node; grown on demand)
+  void* hier_scratch = nullptr;
+  size_t hier_scratch_bytes = 0;
   // host-buffer serving path
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
@@ -213,7 +216,7 @@ cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_sat2_build(nb_grid* g, cudaStream_t s);
 cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* parent, const float* q,
-                       const uint8_t* y, int64_t n, unsigned long long* h_counts, cudaStream_t st,
+                       const uint8_t* y, int64_t n, unsigned long long* h_counts /*[5]*/, cudaStream_t st,
                        cudaError_t (*forward)(const nb_model*, const float*, int64_t,
                                               const unsigned long long*, float*, cudaStream_t));
 

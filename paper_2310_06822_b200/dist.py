@@ -11,13 +11,24 @@ from __future__ import annotations
 import numpy as np
 
 
-def shard(n: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous balanced shard [start, start+count) of n rows for `rank`."""
-    if world < 1 or not 0 <= rank < world or n < 0:
+TILE = 128  # rows per MMA tile; shard starts are tile multiples
+
+
+def shard(n: int, rank: int, world: int, align: int = TILE) -> tuple[int, int]:
+    """Contiguous shard [start, start+count) of n rows for `rank`.
+
+    Starts are multiples of `align` rows (whole 128-row tiles, so every rank's
+    q and y views stay 16-byte aligned for the kernels' bulk copies, nb.h
+    "Alignment"); the tiles are balanced (counts differ by at most one tile)
+    and the last rank takes the ragged tail."""
+    if world < 1 or not 0 <= rank < world or n < 0 or align < 1:
         raise ValueError("bad shard arguments")
-    base, extra = divmod(n, world)
-    start = rank * base + min(rank, extra)
-    return start, base + (1 if rank < extra else 0)
+    tiles = -(-n // align)
+    base, extra = divmod(tiles, world)
+    t0 = rank * base + min(rank, extra)
+    t1 = t0 + base + (1 if rank < extra else 0)
+    start, end = min(n, t0 * align), min(n, t1 * align)
+    return start, end - start
 
 
 def comm_init(model, group=None) -> None:

@@ -20,3 +20,19 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0 and line["gpu_launches"] == 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
     assert line["metric"] == "bounding queries/s" and line["higher_is_better"] is True
+
+
+def test_gpus_2_spawns_two_ranks():
+    """bench.py --gpus 2 without torchrun re-launches itself with two ranks
+    (torch.distributed.run, 127.0.0.1); the dry run (gloo, no GPU work) shows
+    the world every rank joined and the tile-aligned strong-scaling shards of
+    the default c5 step."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["ranks"] == [0, 1]
+    assert line["config"] == "c5" and line["scaling"] == "strong"
+    (s0, c0), (s1, c1) = line["shards"]
+    assert s0 == 0 and s1 == c0 and c0 + c1 == 1 << 28 and s1 % 128 == 0

@@ -70,7 +70,9 @@ def test_shard_partition():
             assert sum(c for _, c in parts) == n
             for (s, c), (s2, _) in zip(parts, parts[1:]):
                 assert s + c == s2
-            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+            assert all(s % 128 == 0 or c == 0 for s, c in parts)   # tile-aligned starts
+            tiles = [-(-c // 128) for _, c in parts]
+            assert max(tiles) - min(tiles) <= 1                       # balanced in tiles
 
 
 def test_float_key_order_preserving():

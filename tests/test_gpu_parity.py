@@ -993,3 +993,84 @@ def test_bf16_sine_with_exit_heads():
     co = oracle.score(ze[keep], y[keep], te)
     for k in ("tp", "fp", "fn", "tn", "exit_hist"):
         assert cg[k] == co[k], (k, cg, co)
+
+
+# ---------------------------------------------------------------- data-parallel semantics (§8(e))
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_two_shards_equal_one_call(name):
+    """libnb's data-parallel semantics on one GPU: two models
+    holding the same parameters each take one contiguous shard (dist.shard,
+    tile-aligned) and the host combines what NCCL would: tau = min of the
+    shard minima, counts = sum, gradient = sum of the shard gradients with
+    each shard normalised by n_global.  Thresholds and counts equal the one
+    full call bit for bit; the summed gradient equals the full-batch gradient
+    up to fp32 summation order, the loss and batch counts likewise."""
+    from paper_2310_06822_b200.dist import shard
+    cfg = nbgen.CONFIGS[name]
+    n = 128 * 148 * 2 + 333
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    th = scaled_params(cfg, 12)
+    full = nb.Model(desc_of(cfg), DEV)
+    full.set_params(th)
+    tau = full.calibrate(qd, yd)
+    c = full.score(qd, yd)
+    parts = [shard(n, r, 2) for r in range(2)]
+    ms = []
+    for s0, cnt in parts:
+        m = nb.Model(desc_of(cfg), DEV)
+        m.set_params(th)
+        ms.append(m)
+    taus = [m.calibrate(qd[s0:s0 + cnt], yd[s0:s0 + cnt]) for m, (s0, cnt) in zip(ms, parts)]
+    tg = torch.minimum(taus[0], taus[1])
+    assert torch.equal(tg, tau)
+    tot = dict(tp=0, fp=0, fn=0, tn=0)
+    for m, (s0, cnt) in zip(ms, parts):
+        m.set_thresholds(tg)
+        cs = m.score(qd[s0:s0 + cnt], yd[s0:s0 + cnt])
+        for k in tot:
+            tot[k] += cs[k]
+    assert tot == {k: c[k] for k in tot} and tot["fn"] == 0
+    # one data-parallel training step: shard gradients normalised by n_global
+    B = 128 * 40 + 77
+    qt = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, B)
+    yt = labels_oracle(cfg, qt.numpy())
+    qtd, ytd = cuda(qt), cuda(yt)
+    full.set_params(th)
+    sf = full.train_step(qtd, ytd, alpha=30.0, stats=True)
+    gf = full.get_grad().double().numpy()
+    gs, ss = np.zeros_like(gf), dict(loss=0.0, tp=0, fp=0, fn=0, tn=0)
+    for m, (s0, cnt) in zip(ms, [shard(B, r, 2) for r in range(2)]):
+        m.set_params(th)
+        st = m.train_step(qtd[s0:s0 + cnt], ytd[s0:s0 + cnt], alpha=30.0, n_global=B, stats=True)
+        gs += m.get_grad().double().numpy()
+        for k in ss:
+            ss[k] += st[k]
+    assert all(ss[k] == sf[k] for k in ("tp", "fp", "fn", "tn"))
+    assert abs(ss["loss"] - sf["loss"]) <= 1e-5 * abs(sf["loss"])
+    assert np.linalg.norm(gs - gf) <= 1e-5 * np.linalg.norm(gf)
+
+
+def test_misaligned_views_rejected_aligned_offsets_work():
+    """nb.h "Alignment": a q/y view that is not 16-byte aligned (row 1 of a
+    contiguous tensor) is rejected with NB_E_ARG before any launch (no
+    misaligned bulk copy can fault the context); a 16-row offset works and
+    equals the same rows copied to a fresh allocation."""
+    cfg = nbgen.CONFIGS["c2"]
+    n = 128 * 30 + 5
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(scaled_params(cfg, 2))
+    m.calibrate(qd, yd)
+    for call in (lambda: m.forward(qd[1:]), lambda: m.score(qd[1:], yd[1:]),
+                 lambda: m.score(qd[:n - 1], yd[1:]), lambda: m.calibrate(qd[3:], yd[3:]),
+                 lambda: m.train_step(qd[1:], yd[1:], alpha=2.0)):
+        with pytest.raises(nb.NBError) as ei:
+            call()
+        assert ei.value.status == 1  # NB_E_ARG
+    assert m.score(qd[16:], yd[16:]) == m.score(qd[16:].clone(), yd[16:].clone())
+    assert torch.equal(m.forward(qd[16:]), m.forward(qd[16:].clone()))
+    torch.cuda.synchronize()   # the context is healthy

@@ -132,3 +132,36 @@ def test_gpu_hierarchy_argument_checks_and_fp32_nodes():
     assert (sub["tp"], sub["fp"], sub["fn"], sub["tn"]) == (int((p & yy).sum()), int((p & ~yy).sum()),
                                                             int((~p & yy).sum()), int((~p & ~yy).sum()))
     assert c["tp"] + c["fp"] + c["fn"] + c["tn"] == n
+
+
+@pytest.mark.gpu
+def test_gpu_hierarchy_nonfinite_and_scratch_reuse():
+    """Non-finite records fail the node that sees them and are reported
+    (warning-class NB_E_NONFINITE with the counts written); repeated calls
+    reuse the root's scratch and give identical counts."""
+    import paper_2310_06822_b200 as nb
+    from gpu_helpers import grid_of
+    cfg = nbgen.CONFIGS["c1"]
+    n = 5000
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = oracle.label(grid_of(cfg), 2, "point", q.numpy())
+    a = oracle.make_arch(2, 64, 3)
+    models = []
+    for i in range(3):
+        m = nb.Model(nb.Desc("point", 2, 64, 3, (), "bf16"), 0)
+        m.set_params(torch.from_numpy(np.random.default_rng(20 + i).normal(size=oracle.num_params(a)) * 0.25).float())
+        m.set_thresholds([-1e9])   # every finite row passes every node
+        models.append(m)
+    yd = torch.from_numpy(y).cuda()
+    ref = nb.hier_score(models, [-1, 0, 0], q.cuda(), yd)
+    assert ref == nb.hier_score(models, [-1, 0, 0], q.cuda(), yd)
+    assert ref["tp"] + ref["fp"] == n and ref["nonfinite"] == 0
+    bad = q.clone()
+    rows = [0, 777, n - 1]
+    bad[rows, 1] = float("nan")
+    with pytest.raises(nb.NBError) as ei:
+        nb.hier_score(models, [-1, 0, 0], bad.cuda(), yd)
+    assert "NONFINITE" in str(ei.value)
+    c = nb.hier_score(models, [-1, 0, 0], bad.cuda(), yd, allow_nonfinite=True)
+    assert c["nonfinite"] == len(rows)
+    assert c["tp"] + c["fp"] == n - len(rows) and c["tp"] + c["fp"] + c["fn"] + c["tn"] == n
