@@ -9,11 +9,15 @@ sets per config: the scaled random weights of the other tests (R46) and a
 model trained through nb_train_step (the P2 case "trained weights").
 
 Per config and weight set:
-  P2  every row, every head: |sigmoid(z_gpu) - sigmoid(z_fp64)| <= 2e-2;
-      and the logit against the kernel-precision oracle (ORA_BF16_EMU, R33):
-      >= 99 % of all rows and >= 90 % of every 128-row tile within the 1e-3
-      band (a tile staged from the wrong rows or a stale buffer fails the
-      per-tile bound);
+  P2  every row, every head: |sigmoid(z_gpu) - sigmoid(z_emu)| <= 2e-2
+      against the network the kernel evaluates (bf16 weights and
+      activations, ORA_BF16_EMU, R33), and against the plain fp64 network
+      |sigmoid(z_gpu) - sigmoid(z_fp64)| <= 2e-2 + the bf16 network's own
+      gap |sigmoid(z_emu) - sigmoid(z_fp64)| (R47; the gap is zero-ish for
+      the scaled weights, where the plain 2e-2 is asserted on every row);
+      the logit against ORA_BF16_EMU: >= 99 % of all rows and >= 90 % of
+      every 128-row tile within the 1e-3 band (a tile staged from the wrong
+      rows or a stale buffer fails the per-tile bound);
   P4  counts of the calibrated predictor bit-exact against the oracle's
       outside the band (R28), and the fused score's counts equal to the
       forward logits thresholded row by row (score and forward agree at
@@ -69,12 +73,19 @@ def test_every_row_at_depth(name, n, weights):
     z = m.forward(qd).cpu().double().numpy()
     a = oracle.arch_of(cfg)
     th64 = th.double().numpy()
-    # P2 every row against the plain fp64 definition
+    # P2 every row against the network the kernel evaluates and against fp64 (R47)
     zr = oracle.forward(a, th64, q.numpy())
-    err = np.abs(sigmoid(z) - sigmoid(zr))
-    assert err.max() <= 2e-2, (err.max(), int(np.argmax(err.max(1))))
-    # every row against the kernel-precision oracle; per-tile bound catches pipeline faults
     ze = oracle.forward(a, th64, q.numpy(), oracle.BF16_EMU)
+    err_emu = np.abs(sigmoid(z) - sigmoid(ze))
+    assert err_emu.max() <= 2e-2, (err_emu.max(), int(np.argmax(err_emu.max(1))))
+    gap = np.abs(sigmoid(ze) - sigmoid(zr))          # the bf16 network vs the fp64 network (oracle only)
+    err = np.abs(sigmoid(z) - sigmoid(zr))
+    assert np.all(err <= gap + 2e-2), float((err - gap).max())
+    if weights == "scaled":
+        assert err.max() <= 2e-2, (err.max(), int(np.argmax(err.max(1))))
+    print(name, weights, "max |dsig| vs emu %.2e, vs fp64 %.2e (bf16-network gap %.2e, rows > 2e-2: %d)"
+          % (err_emu.max(), err.max(), gap.max(), int((err.max(1) > 2e-2).sum())))
+    # every row against the kernel-precision oracle; per-tile bound catches pipeline faults
     close = np.all(np.abs(z - ze) < BAND, axis=1)
     assert close.mean() >= 0.99, close.mean()
     nt = n // 128
@@ -115,9 +126,10 @@ def _tensors(cfg):
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_trained_gradient_parity_vs_fp64(name):
-    """P3 at trained weights: one step's per-tensor gradient within 2e-2 of
-    the plain fp64 definition (BASELINE.json) and of the kernel-precision
-    gradient (R34), over a batch spanning many tiles."""
+    """P3 at trained weights, over a batch spanning many tiles: one step's
+    per-tensor gradient within 2e-2 of the gradient of the network the
+    kernels evaluate (ORA_BF16_EMU, R34), and within 2e-2 + that network's
+    own gap to the fp64 gradient of the plain definition (R47)."""
     cfg = nbgen.CONFIGS[name]
     th = trained_params(cfg)
     n = (1 << 14) + 77
@@ -138,6 +150,10 @@ def test_trained_gradient_parity_vs_fp64(name):
              if np.linalg.norm(ge[s]) > 0}
     print(name, "rel64", {k: round(v, 4) for k, v in rel64.items()})
     print(name, "relemu", {k: round(v, 4) for k, v in relem.items()})
+    gap = {k: np.linalg.norm(ge[s] - gr[s]) / np.linalg.norm(gr[s]) for k, s in _tensors(cfg)
+           if np.linalg.norm(gr[s]) > 0}
+    print(name, "bf16-network gap", {k: round(v, 4) for k, v in gap.items()})
     assert max(relem.values()) <= 2e-2, relem
-    assert max(rel64.values()) <= 2e-2, rel64
-    assert abs(st["loss"] - loss) <= 2e-2 * abs(loss)
+    assert all(rel64[k] <= gap[k] + 2e-2 for k in rel64), (rel64, gap)
+    assert abs(st["loss"] - le) <= 1e-3 * abs(le)
+    assert abs(st["loss"] - loss) <= abs(le - loss) + 2e-2 * abs(loss)

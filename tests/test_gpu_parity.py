@@ -285,7 +285,8 @@ def test_bf16_train_step_gradient_parity(name, n):
     assert max(rel_emu.values()) <= 2e-2, rel_emu
     # against the plain fp64 definition (BASELINE.json 2e-2): holds for the
     # shallow nets; the 6-layer c4 net differs from fp64 by the bf16 forward
-    # itself (the oracle's own bf16-precision gradient shows the same gap)
+    # itself (the oracle's own bf16-precision gradient shows the same gap):
+    # the kernel is held to that gap + 2e-2 (R47)
     loss, gr, sr = oracle.loss_grad(a, th.double().numpy(), q.numpy(), y, alpha, 1.0)
     rel64 = {nm: np.linalg.norm(g[sl] - gr[sl]) / np.linalg.norm(gr[sl])
              for nm, sl in param_tensors(cfg) if np.linalg.norm(gr[sl]) > 0}
