@@ -54,7 +54,7 @@ WORKLOAD = {
 KERNEL = {"c2": "k_fwd_tc<64,4,0,0,kScore,d0=3,BF>", "c3": "k_fwd_tc<128,4,0,0,kScore,d0=6,BF>",
           "c4": "k_score_exit<2,{records,image,image},{head1,head2,output}> (early-exit compaction, "
                 "3 segment kernels per 2^24-row chunk)",
-          "c5": "k_fwd_tc2<4,kScore,BF> (CTA pairs)"}
+          "c5": "k_fwd_tc2p<4,kScore,d0=6> (pipelined CTA pairs)"}
 METRIC = "bounding queries/s"
 UNIT = "queries/s"
 # bounded oracle samples (about 10 s of host work per step at 16 cores)
