@@ -42,7 +42,7 @@ SOURCES = {
     "nb_label.cu": ["-fmad=false"],   # exact fp64 DDA rounding (no FMA contraction)
     "nb_comm.cpp": [],
 }
-HEADERS = ["nb_internal.cuh", "nb_device.cuh", "nb_fwd_tc.cuh"]
+HEADERS = ["nb_internal.cuh", "nb_device.cuh", "nb_fwd_tc.cuh", "nb_adam.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

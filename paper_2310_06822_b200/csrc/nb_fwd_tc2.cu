@@ -223,7 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
     tc_fence_before();
     asm volatile("bar.sync 1, 512;" ::: "memory");
     if (warp == 0) {
-      if (lane == 0) mbar_arrive_remote(a_full_leader);
+      if (lane == 0) mbar_arrive_remote_cta(a_full_leader);
       if (leader) {
         while (!mbar_try_wait_cluster(a_full, aph)) {
         }

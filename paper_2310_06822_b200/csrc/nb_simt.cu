@@ -7,6 +7,7 @@
 // §3.3 early-out P:231-279, §3.4 P:285-297.
 #include <cuda_bf16.h>
 
+#include "nb_adam.cuh"
 #include "nb_device.cuh"
 #include "nb_internal.cuh"
 
@@ -62,26 +63,6 @@ cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* ou
 // Layer 1's K = 16 image holds W_1 twice: columns [0, d0) multiply the hi
 // halves, [d0, 2 d0) the lo halves of the encoded input.
 // ---------------------------------------------------------------------------
-struct PackArgs {
-  const float* theta;
-  uint8_t* out;
-  uint8_t* out_bwd;  // transposed pair images (w = 256) or NULL
-  BwdLayout bl;
-  PackLayout pl;
-  ParamOffsets po;
-  int W, L, d0, nh;
-};
-
-// Piece j of the exact three-way bf16 split b = hi + mid + lo (each piece is
-// exactly representable in bf16; their fp32 sum is b for normal-range b).
-__device__ __forceinline__ float bias_piece(float b, int j) {
-  const float hi = __bfloat162float(__float2bfloat16_rn(b));
-  const float r = b - hi;
-  const float mid = __bfloat162float(__float2bfloat16_rn(r));
-  const float lo = __bfloat162float(__float2bfloat16_rn(r - mid));
-  return j == 0 ? hi : (j == 1 ? mid : lo);
-}
-
 __global__ void k_pack_bf16(PackArgs a) {
   const int W = a.W;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -647,13 +628,6 @@ cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int
 
 // ---------------------------------------------------------------------------
 // Adam (PyTorch semantics, R8) on the fp32 master weights.
-// ---------------------------------------------------------------------------
-// L1 + L2 regularisation (Suppl. §2.2; R38): the
-// gradient of l1 * sum |theta| + l2 * sum theta^2 over all parameters.
-__device__ __forceinline__ float reg_grad(float t, float l1, float l2) {
-  return l1 * (t > 0.f ? 1.f : (t < 0.f ? -1.f : 0.f)) + 2.f * l2 * t;
-}
-
 __global__ void k_adam(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, int64_t P, float lr_over_bc1,
                        float inv_sqrt_bc2, float b1, float b2, float eps, float l1, float l2) {
@@ -668,84 +642,13 @@ __global__ void k_adam(float* __restrict__ th, float* __restrict__ m, float* __r
   }
 }
 
-// Adam fused with the bf16 re-pack: the thread that updates parameter i also
-// writes every packed copy of it (weight image element(s), fp32 tail entries,
-// bias split pieces) — the same values k_pack_bf16 would write; padding
-// positions of the image never change after the first full pack.
-__device__ __forceinline__ void store_bf16(uint8_t* img, int K, int n, int k, float v) {
-  reinterpret_cast<__nv_bfloat16*>(img)[(int64_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 +
-                                        (k % 8)] = __float2bfloat16_rn(v);
-}
-
+// Adam fused with the bf16 re-pack (nb_adam.cuh adam_pack_one): the thread
+// that updates parameter i also writes every packed copy of it.
 __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
-                            const float* __restrict__ g, int64_t P, float lr_over_bc1,
-                            float inv_sqrt_bc2, float b1, float b2, float eps, float l1, float l2,
-                            PackArgs a) {
-  const int W = a.W, rows = W / (int)a.pl.pairs;
+                            const float* __restrict__ g, int64_t P, AdamArgs h, PackArgs a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i] + reg_grad(th[i], l1, l2);
-    const float mi = b1 * m[i] + (1.f - b1) * gi;
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    const float t = th[i] - lr_over_bc1 * mi / (sqrtf(vi) * inv_sqrt_bc2 + eps);
-    th[i] = t;
-    // ---- re-pack parameter i
-    auto fp32_tail = [&](uint32_t off_bytes) {  // replicated in every pair image
-      for (uint32_t im = 0; im < a.pl.pairs; ++im)
-        *reinterpret_cast<float*>(a.out + (size_t)im * a.pl.bytes + off_bytes) = t;
-    };
-    bool done = false;
-    for (int l = 0; l < a.L && !done; ++l) {
-      const int in = l == 0 ? a.d0 : W;
-      const int64_t ow = a.po.W[l], ob = a.po.b[l];
-      if (i >= ow && i < ow + (int64_t)W * in) {
-        const int n = (int)((i - ow) / in), k = (int)((i - ow) % in);
-        uint8_t* img = a.out + (size_t)(n / rows) * a.pl.bytes + a.pl.off_w[l];
-        store_bf16(img, (int)a.pl.k_of[l], n % rows, k, t);
-        if (l == 0)  // lo copy (after hi, or at pe_lo for PE nets)
-          store_bf16(img, (int)a.pl.k_of[0], n % rows, (a.pl.pe_lo ? (int)a.pl.pe_lo : a.d0) + k, t);
-        if (l > 0 && a.out_bwd)  // transposed pair image: row = input feature k, column = n
-          store_bf16(a.out_bwd + (size_t)(k / rows) * a.bl.bytes + a.bl.off_wt[l], W, k % rows, n, t);
-        done = true;
-      } else if (i >= ob && i < ob + W) {
-        const int n = (int)(i - ob);
-        fp32_tail(a.pl.off_bias + 4u * (uint32_t)(l * W + n));
-        uint8_t* imgb = a.out + (size_t)(n / rows) * a.pl.bytes;  // the image holding row n
-        if (l == 0 && a.pl.bias_l0) {
-          for (int j = 0; j < 3; ++j)
-            store_bf16(imgb + a.pl.off_w[0], (int)a.pl.k_of[0], n % rows,
-                       (a.pl.pe_lo ? 1 : 2) * a.d0 + j, bias_piece(t, j));
-        } else if (l > 0 && a.pl.bb_shared) {
-          for (int j = 0; j < 3; ++j)
-            store_bf16(imgb + a.pl.off_bb[0], kEncK, n % rows, 3 * (l - 1) + j, bias_piece(t, j));
-        } else if (l > 0 && a.pl.off_bb[l]) {
-          for (int j = 0; j < 3; ++j) store_bf16(a.out + a.pl.off_bb[l], kEncK, n, j, bias_piece(t, j));
-        }
-        done = true;
-      }
-    }
-    if (done) continue;
-    auto bwd_tail = [&](uint32_t off_bytes) {
-      if (a.out_bwd)
-        for (int im = 0; im < 2; ++im) *reinterpret_cast<float*>(a.out_bwd + (size_t)im * a.bl.bytes + off_bytes) = t;
-    };
-    if (i >= a.po.wout && i < a.po.wout + W) {
-      fp32_tail(a.pl.off_wout + 4u * (uint32_t)(i - a.po.wout));
-      bwd_tail(a.bl.off_wout + 4u * (uint32_t)(i - a.po.wout));
-    } else if (i == a.po.bout) {
-      fp32_tail(a.pl.off_bout);
-    }
-    for (int k = 0; k < a.nh; ++k) {
-      if (i >= a.po.u[k] && i < a.po.u[k] + W) {
-        fp32_tail(a.pl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
-        bwd_tail(a.bl.off_u[k] + 4u * (uint32_t)(i - a.po.u[k]));
-      } else if (i == a.po.c[k]) {
-        fp32_tail(a.pl.off_c + 4u * (uint32_t)k);
-      }
-    }
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    adam_pack_one(i, g[i], th, m, v, h, a);
 }
 
 cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
@@ -763,10 +666,9 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
   a.L = m->d.hidden_layers;
   a.d0 = m->din;
   a.nh = m->d.n_heads;
+  AdamArgs h{(float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1, (float)b2, (float)eps, m->l1, m->l2};
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
-  k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P,
-                                     (float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1,
-                                     (float)b2, (float)eps, m->l1, m->l2, a);
+  k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P, h, a);
   return cudaGetLastError();
 }
 
