@@ -739,13 +739,13 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   }
   NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
   if (tc)
-    NB_CUDA(launch_train_tc(m, q, y, n_local, n_global, alpha, beta, lr, s));
+    NB_CUDA(launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s));
   else
     NB_CUDA(launch_train_simt(m, q, y, n_local, n_global, alpha, beta, s));
   if (m->comm) {
     if (comm_allreduce_f32_sum(m, m->grad, m->P, s)) return NB_E_NCCL;
   }
-  if (tc && !m->step_finalized) NB_CUDA(launch_adam_pack(m, lr, s));
+  if (tc) NB_CUDA(launch_adam_pack(m, lr, s));
   else NB_CUDA(launch_adam(m, lr, s));
   if (stats) {
     if (m->comm) {

@@ -24,7 +24,6 @@ constexpr int kNumCounters = 9;     // tp fp fn tn exit[4] nonfinite
 constexpr int kCtrStride = 16;      // device counters 128 B apart (one L2 line each); set 1 at +8
 constexpr int kFinOff = kNumCounters * kCtrStride;  // nb_model::d_counts: finalised totals
 constexpr int kZeroOff = kFinOff + 16;              // ... and a block that stays zero
-constexpr int kGridBarOff = 200;                    // fused training: grid-barrier arrival counter
 constexpr uint32_t kFlagNonFinite = 1u, kFlagLabel = 2u;
 
 void set_error(const char* fmt, ...);
@@ -108,8 +107,6 @@ struct nb_model {
   // training scratch (grown on demand outside the timed hot path)
   void* train_scratch = nullptr;
   size_t train_scratch_bytes = 0;
-  unsigned long long gbar_count = 0;  // host shadow of the fused kernel's grid-barrier counter
-  int step_finalized = 0;             // the last launch_train_tc also applied Adam + re-pack
   // early-exit compaction scratch (nb_fwd_exit.cu): 2 image/label region sets
   void* exit_scratch = nullptr;
   size_t exit_scratch_bytes = 0;
@@ -205,7 +202,7 @@ bool simt_supported(const nb_desc& d);
 cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                               int64_t n_global, float alpha, float beta, cudaStream_t s);
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
-                            int64_t n_global, float alpha, float beta, float lr, cudaStream_t s);
+                            int64_t n_global, float alpha, float beta, cudaStream_t s);
 bool train_tc_supported(const nb_desc& d);
 cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8_t* const* d_img,
                            const float* g32, int64_t n, cudaStream_t st);

@@ -13,12 +13,10 @@
 //             TMEM over all of the CTA's tiles; the head's dz^T [h_L | 1] rides
 //             in row 64 of the last layer's delta image.
 // At the end each CTA writes its dW accumulators as partials in the layout of
-// nb_train_tc.cu's k_dw_tc.  Without a communicator the same launch (a
-// cooperative grid) then finishes the step: a grid barrier, a fixed-order
-// reduction of the partials into the gradient (4 CTA slices per parameter,
-// combined in a fixed tree: deterministic) and Adam + bf16 re-pack of each
-// parameter by the thread that reduced it (nb_adam.cuh).  With a
-// communicator, k_dw_reduce -> NCCL allreduce -> k_adam_pack follow instead.
+// nb_train_tc.cu's k_dw_tc; k_dw_reduce (fixed order), the NCCL allreduce
+// (with a communicator) and k_adam_pack follow.  (Finishing the step inside
+// this launch — grid barrier, reduce, Adam + re-pack — was measured slower
+// than the two short launches: 53 vs 45 us per c2 step.)
 // The backward issues g_{l-1} = delta_l W_l first and commits it on its own
 // barrier, so the next layer's delta epilogue starts while the dW MMAs of
 // layer l still run (they commit to dw_bar, waited before the delta image is
@@ -30,7 +28,6 @@
 #include <cmath>
 #include <cstring>
 
-#include "nb_adam.cuh"
 #include "nb_fwd_tc.cuh"
 
 namespace nb {
@@ -47,18 +44,6 @@ struct FusedParams {
   unsigned long long* stats;
   unsigned int* flags;
   float* partial;  // [job][cta][kDwColsF][128]
-  // in-kernel finalisation (no communicator): grid barrier, reduce, Adam + re-pack
-  int finalize;
-  unsigned long long* gbar;          // monotone arrival counter
-  unsigned long long gbar_target;    // its value once every CTA of this launch arrived
-  float* grad;
-  float* th;
-  float* am;
-  float* av;
-  int64_t P;
-  ParamOffsets po;
-  AdamArgs ha;
-  PackArgs pa;
 };
 constexpr int kFusedW = 64;
 constexpr int kDwColsF = 272;  // = nb_train_tc.cu kDwCols
@@ -373,81 +358,6 @@ __global__ void __launch_bounds__(256, 1) k_train_fused(const FusedParams p) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
-  if (!p.finalize) return;
-  // ---------------- grid barrier (cooperative launch: all CTAs resident) ----------------
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(p.gbar, 1ull);
-    unsigned long long v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.gbar) : "memory");
-      if (v < p.gbar_target) __nanosleep(64);
-    } while (v < p.gbar_target);
-  }
-  __syncthreads();
-  // ---------------- fixed-order reduction + Adam + re-pack ----------------
-  // parameter i -> (job, D row, partial columns): W_1 / b_1 job 0 (hi + lo
-  // columns j and d0 + j, bias column 16), W_l / b_l job l (bias column 64),
-  // w_out / b_out the head job (D row 64).  Eight lanes per parameter sum the
-  // CTA slices [s per, (s + 1) per) in order, then the slice sums in order
-  // 0..7: exactly k_dw_reduce's tree, so the gradient is bit-identical to the
-  // unfused path (and to the communicator path at world size 1).
-  constexpr int kMaxPer = 19;  // ceil(148 / 8)
-  const int G = gridDim.x;
-  const int per = (G + 7) / 8;
-  const int slot = lane >> 3, sl = lane & 7;
-  const int64_t cs = (int64_t)kDwColsF * 128;
-  for (int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 4; base < p.P; base += (int64_t)G * 32) {
-    const int64_t i = base + slot;
-    int job = -1, m = 0, c0 = 0, c1 = -1;
-    if (i < p.P) {
-      if (i < p.po.b[0]) {
-        const int64_t e = i - p.po.W[0];
-        job = 0; m = (int)(e / d0); c0 = (int)(e % d0); c1 = d0 + c0;
-      } else if (i < p.po.b[0] + W) {
-        job = 0; m = (int)(i - p.po.b[0]); c0 = 16;
-      }
-      for (int l = 1; l < L && job < 0; ++l) {
-        if (i >= p.po.W[l] && i < p.po.b[l]) {
-          const int64_t e = i - p.po.W[l];
-          job = l; m = (int)(e / W); c0 = (int)(e % W);
-        } else if (i >= p.po.b[l] && i < p.po.b[l] + W) {
-          job = l; m = (int)(i - p.po.b[l]); c0 = 64;
-        }
-      }
-      if (job < 0) {  // output head
-        job = L; m = 64;
-        c0 = i == p.po.bout ? 64 : (int)(i - p.po.wout);
-      }
-    }
-    float acc = 0.f;
-    if (job >= 0) {
-      const float* P0 = p.partial + (int64_t)job * G * cs + (int64_t)c0 * 128 + m;
-      const int cb = sl * per, ce = min(G, cb + per);
-      float x[kMaxPer], yv[kMaxPer];
-#pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        const bool ok = cb + u < ce;
-        x[u] = ok ? __ldcg(P0 + (int64_t)(cb + u) * cs) : 0.f;
-        yv[u] = (ok && c1 >= 0) ? __ldcg(P0 + (int64_t)(cb + u) * cs + (int64_t)(c1 - c0) * 128) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        if (cb + u < ce) {
-          acc += x[u];
-          if (c1 >= 0) acc += yv[u];
-        }
-      }
-    }
-    // slice sums in order 0..7 (lane 8 slot gathers)
-    float tot = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) tot += __shfl_sync(0xFFFFFFFFu, acc, (lane & ~7) + q);
-    if (sl == 0 && job >= 0) {
-      p.grad[i] = tot;
-      adam_pack_one(i, tot, p.th, p.am, p.av, p.ha, p.pa);
-    }
-  }
 }
 
 bool train_fused_supported(const nb_model* m) {
@@ -464,7 +374,7 @@ size_t train_fused_smem(const nb_model* m) {
 
 cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                                int64_t n_global, float alpha, float beta, float* partial,
-                               int* cpj, bool finalize, float lr, cudaStream_t st) {
+                               int* cpj, cudaStream_t st) {
   FusedParams p;
   memset(&p, 0, sizeof(p));
   p.packed = m->packed;
@@ -488,37 +398,8 @@ cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, in
   auto kern = p.L == 4 ? k_train_fused<4> : k_train_fused<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (!finalize) {
-    kern<<<grid, 256, smem, st>>>(p);
-    return cudaGetLastError();
-  }
-  // the step's Adam + re-pack inside the launch (nb_adam.cuh): bias corrections of step t
-  m->step += 1;
-  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-  const double bc1 = 1.0 - pow(b1, (double)m->step), bc2 = 1.0 - pow(b2, (double)m->step);
-  p.finalize = 1;
-  p.gbar = m->d_counts + kGridBarOff;
-  m->gbar_count += (unsigned long long)grid;
-  p.gbar_target = m->gbar_count;
-  p.grad = m->grad;
-  p.th = m->theta;
-  p.am = m->adam_m;
-  p.av = m->adam_v;
-  p.P = m->P;
-  p.po = m->po;
-  p.ha = AdamArgs{(float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1, (float)b2, (float)eps, m->l1, m->l2};
-  p.pa.theta = m->theta;
-  p.pa.out = m->packed;
-  p.pa.out_bwd = m->packed_bwd;
-  p.pa.bl = m->bl;
-  p.pa.pl = m->pl;
-  p.pa.po = m->po;
-  p.pa.W = m->d.width;
-  p.pa.L = m->d.hidden_layers;
-  p.pa.d0 = m->din;
-  p.pa.nh = m->d.n_heads;
-  void* args[] = {&p};
-  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st);
+  kern<<<grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
 }
 
 }  // namespace nb

@@ -555,7 +555,7 @@ cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaSt
 bool train_fused_supported(const nb_model* m);
 cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                                int64_t n_global, float alpha, float beta, float* partial,
-                               int* cpj, bool finalize, float lr, cudaStream_t st);
+                               int* cpj, cudaStream_t st);
 
 // One micro-batch: forward (kTrain) + backward chain + dW GEMMs (partials
 // written when `first`, accumulated otherwise).
@@ -617,8 +617,7 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
 }
 
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
-                            int64_t n_global, float alpha, float beta, float lr, cudaStream_t st) {
-  m->step_finalized = 0;
+                            int64_t n_global, float alpha, float beta, cudaStream_t st) {
   const int W = m->d.width, L = m->d.hidden_layers, d0 = m->d0;
   const int64_t chunk = train_chunk_rows(m, n);
   TrainLayout tl = train_layout(m, chunk, m->num_sms);
@@ -633,16 +632,8 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
       fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 0, W, 0, d0, W, g + m->po.W[l], g + m->po.b[l]};
     // the head gradient rides in row 64 of the last layer's delta image
     fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
-    // in-kernel finalisation (grid barrier, reduce, Adam + re-pack in the same
-    // launch) measured slower than the two short launches (c2: 53 vs 45 us per
-    // step): off unless NB_FUSED_FINALIZE is set (measurement switch)
-    const bool fin = !m->comm && getenv("NB_FUSED_FINALIZE");
-    cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, fin, lr, st);
+    cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, st);
     if (e != cudaSuccess) return e;
-    if (fin) {
-      m->step_finalized = 1;
-      return cudaSuccess;
-    }
     return launch_dw_reduce(fj, st);
   }
   // dW jobs (image pointers are the same for every micro-batch)
