@@ -632,6 +632,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
     if (bias0) encode_cols2<true>(x, d0, c);
     else encode_cols2<false>(x, d0, c);
     tmem_st8(trow + acol(abuf), c);
+    if (MODE == kTrain && 2 * t + rank < p.a.tr.num_tiles) {  // layer-1 input image (dW GEMM)
+      uint8_t* base = p.a.tr.x_img + (2 * t + rank) * img_tile_bytes(16);
+#pragma unroll
+      for (int fg = 0; fg < 2; ++fg)
+        *reinterpret_cast<uint4*>(base + (fg * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+            make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+    }
   };
   // end of this warp's part of one half's epilogue (its D columns read, its A
   // columns written): one arrive per warp on the leader's barrier, no CTA-wide
@@ -753,12 +760,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
               add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
             }
           }
-          if (!last) {
+          if (!last || MODE == kTrain) {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
-            tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
-          } else {
+            if (!last) tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
+            if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
+              uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4)
+                *reinterpret_cast<uint4*>(base + ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                    make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            }
+          }
+          if (last) {
             const float* wo = wout + f0;
 #pragma unroll
             for (int i = 0; i < CPT; i += 2)
@@ -802,6 +817,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
             if (p.a.prob) p.a.prob[r] = 1.f / (1.f + __expf(-z));
             if (!isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
           }
+        } else if (MODE == kTrain) {
+          // Eq. (1): w = alpha if y else beta, term w softplus(-+z),
+          // dL/dz = w (sigmoid(z) - y) / B (R4, R5); batch counts at z >= 0 (R31)
+          const float w = valid ? (yv ? p.a.tr.alpha : p.a.tr.beta) : 0.f;
+          const float sp = fmaxf(yv ? -z : z, 0.f) + log1pf(__expf(-fabsf(z)));
+          float lsum = w * sp;
+          const float gz = w * (1.f / (1.f + __expf(-z)) - (float)yv) * p.a.tr.inv_b;
+          if (valid) {
+            p.a.tr.g32[r * 3] = gz;
+            p.a.tr.g32[r * 3 + 1] = 0.f;
+            p.a.tr.g32[r * 3 + 2] = 0.f;
+          }
+          const int64_t rt = 2 * tile + rank;
+          if (rt < p.a.tr.num_tiles)
+            *reinterpret_cast<uint4*>(p.a.tr.hd_img + rt * img_tile_bytes(8) + (row / 8) * 128 + (row % 8) * 16) =
+                make_uint4(pack_bf16x2(gz, 0.f), 0u, 0u, 0u);
+          for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xFFFFFFFFu, lsum, o);
+          const bool pred = z >= 0.f, yy = yv != 0;
+          const uint32_t c0 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
+          const uint32_t c1 = __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
+          const uint32_t c2 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && yy));
+          const uint32_t c3 = __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
+          if (lane == 0) {
+            if (lsum != 0.f) atomicAdd(p.a.tr.loss, (double)lsum * (double)p.a.tr.inv_b);
+            ctr[0] += c0; ctr[1] += c1; ctr[2] += c2; ctr[3] += c3;
+          }
+          if (valid && yv > 1) atomicOr(p.a.flags, kFlagLabel);
         } else if (MODE == kCalibrate) {
           if (valid && !isfinite(z)) atomicOr(p.a.flags, kFlagNonFinite);
           if (valid && (p.a.invert ? yv == 0 : yv == 1)) key = min(key, dkey(p.a.invert ? -z : z));
@@ -826,6 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+  if (MODE == kTrain && warp == 1 && lane < 4 && ctr[lane]) atomicAdd(p.a.tr.stats + lane, (unsigned long long)ctr[lane]);
   if (MODE == kScore && warp == 1) flush_cta_counts(ctr, 1, 0, p.a.counts);
   if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a);
 }
@@ -860,6 +903,7 @@ static cudaError_t launch_tc2p_m(const nb_model* m, const FwdArgs& a, cudaStream
 template <int LC, int D0>
 static cudaError_t launch_tc2p_l(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
   if (mode == kForward) return launch_tc2p_m<LC, kForward, D0>(m, a, st);
+  if (mode == kTrain) return launch_tc2p_m<LC, kTrain, D0>(m, a, st);
   if (mode == kCalibrate) return launch_tc2p_m<LC, kCalibrate, D0>(m, a, st);
   return launch_tc2p_m<LC, kScore, D0>(m, a, st);
 }
@@ -908,7 +952,7 @@ static bool tc2_single() {
 }
 
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
-  if (mode != kTrain && m->d.n_heads == 0 && !tc2_single()) {  // pipelined halves (forward / calibrate / score)
+  if (m->d.n_heads == 0 && !tc2_single()) {  // pipelined halves
     if (m->d.hidden_layers == 4 && m->d0 == 6) return launch_tc2p_l<4, 6>(m, mode, a, st);  // BJ configs[4]
     return launch_tc2p_l<0, 0>(m, mode, a, st);
   }
