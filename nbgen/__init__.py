@@ -125,6 +125,16 @@ CONFIGS = {
 }
 
 
+# NEXT-3: 4D rays, boxes and hyperplanes over c4's animated
+# scene (8-float records, Suppl. Tab. 4/5 "4D Ray, Plane, Box"; R48).  Test and
+# measurement configs beside BASELINE.json's five; net 8 -> 128 x 4 -> 1 bf16.
+EXTRA_CONFIGS = {
+    f"c4{k}": Config(f"c4{k}", 4, k, 128, 4, (), "bf16", 1 << 20, 1 << 16, 5000,
+                     grid=dict(kind="moving_spheres", R=64, frames=32, count=12))
+    for k in ("ray", "box", "plane")
+}
+
+
 def grid_shape(cfg: Config) -> tuple:
     g = cfg.grid
     if g["kind"] == "discs":
@@ -215,11 +225,14 @@ def make_grid(cfg: Config) -> torch.Tensor:
 # --------------------------------------------------------------------------
 DRAWS_PER_ROW = {"point": None, "ray": 5, "box": 6, "plane": 5}
 DRAWS_PER_ROW_2D = {"ray": 3, "box": 4, "plane": 3}  # 2D rays / boxes / lines
+DRAWS_PER_ROW_4D = {"ray": 7, "box": 8, "plane": 7}  # 4D rays / boxes / hyperplanes (NEXT-3, R48)
 
 
 def _draws_per_row(cfg: Config) -> int:
     if cfg.kind == "point":
         return cfg.space_dim
+    if cfg.space_dim == 4:
+        return DRAWS_PER_ROW_4D[cfg.kind]
     return DRAWS_PER_ROW_2D[cfg.kind] if cfg.space_dim == 2 else DRAWS_PER_ROW[cfg.kind]
 
 
@@ -237,6 +250,15 @@ def _unit_dirs(u_z: torch.Tensor, u_phi: torch.Tensor) -> torch.Tensor:
     return torch.stack([r * torch.cos(phi), r * torch.sin(phi), z], dim=1)
 
 
+def _unit_dirs_4d(u1: torch.Tensor, u2: torch.Tensor, u3: torch.Tensor) -> torch.Tensor:
+    """Uniform directions on S^3 (Shoemake's uniform unit quaternions)."""
+    a = torch.sqrt(1.0 - u1.double())
+    b = torch.sqrt(u1.double())
+    t1 = 2.0 * math.pi * u2.double()
+    t2 = 2.0 * math.pi * u3.double()
+    return torch.stack([a * torch.sin(t1), a * torch.cos(t1), b * torch.sin(t2), b * torch.cos(t2)], dim=1)
+
+
 def make_queries(cfg: Config, tag: int, row0: int, n: int, device="cpu") -> torch.Tensor:
     """fp32 [n][record_floats] for rows [row0, row0+n) of stream `tag`."""
     D = _draws_per_row(cfg)
@@ -244,6 +266,28 @@ def make_queries(cfg: Config, tag: int, row0: int, n: int, device="cpu") -> torc
     u = u32f(draws(key, row0 * D, n * D, device)).view(n, D)
     if cfg.kind == "point":
         return u.contiguous()
+    if cfg.space_dim == 4:  # 8-float records over (x, y, z, t) (R48)
+        if cfg.kind == "ray":  # origin on the boundary of [0,1]^4, direction uniform on S^3
+            facet = torch.clamp((u[:, 0].double() * 8.0).floor().long(), max=7)
+            axis, side = facet % 4, (facet // 4).double()
+            o = torch.empty(n, 4, dtype=torch.float64, device=device)
+            free = [u[:, 1].double(), u[:, 2].double(), u[:, 3].double()]
+            for a in range(4):
+                others = [b for b in range(4) if b != a]
+                m = axis == a
+                o[m, a] = side[m]
+                for j, b in enumerate(others):
+                    o[m, b] = free[j][m]
+            d = _unit_dirs_4d(u[:, 4], u[:, 5], u[:, 6])
+            return torch.cat([o, d], 1).to(torch.float32).contiguous()
+        if cfg.kind == "box":  # c5's box recipe with 4 axes
+            lo = u[:, 0:4]
+            e = 0.005 + 0.095 * u[:, 4:8].double()
+            hi = torch.clamp(lo.double() + e, max=1.0).to(torch.float32)
+            return torch.cat([lo, hi], 1).contiguous()
+        if cfg.kind == "plane":  # a point of [0,1]^4 and a unit normal on S^3
+            nrm = _unit_dirs_4d(u[:, 4], u[:, 5], u[:, 6])
+            return torch.cat([u[:, 0:4].double(), nrm], 1).to(torch.float32).contiguous()
     if cfg.space_dim == 2:  # 4-float records: origin on the square's boundary + direction,
         if cfg.kind == "ray":  # lo/hi corners, or a line's point + unit normal
             edge = torch.clamp((u[:, 0].double() * 4.0).floor().long(), max=3)

@@ -370,11 +370,221 @@ static int line2_scan_res(const uint8_t* g, int32_t R, int sub, const double* p0
   return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* 4D (space x time) rays, hyperplanes and boxes (
+ * Suppl. Tab. 4/5 "4D Ray, Plane, Box"; "pairs of Cartesian
+ * nD start- and direction-vectors ... corners ... p0 and normal").
+ * Reading R48: coordinates (x, y, z, t) in [0,1]^4, cells are the half-open
+ * space-time cells [i/R,(i+1)/R) x ... x [f/F,(f+1)/F) of the [F][R][R][R]
+ * grid (the 4D point indicator's cells, R15 per axis); R16, R17 and R19
+ * carry over with 4 axes.                                                 */
+static int res4(int32_t R, int32_t F, int ax) { return ax < 3 ? R : F; }
+
+static int occ4(const uint8_t* g, int32_t R, const int* c) { /* c = (x, y, z, t) cell */
+  return g[(((int64_t)c[3] * R + c[0]) * R + c[1]) * R + c[2]] != 0;
+}
+
+static int ray4_clip(const double* o, const double* d, double* s_in, double* s_out) {
+  double a = 0.0, b = INFINITY;
+  for (int j = 0; j < 4; ++j) {
+    if (d[j] == 0.0) {
+      if (o[j] < 0.0 || o[j] > 1.0) return 0;
+      continue;
+    }
+    double t0 = (0.0 - o[j]) / d[j], t1 = (1.0 - o[j]) / d[j];
+    if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+    if (t0 > a) a = t0;
+    if (t1 < b) b = t1;
+  }
+  *s_in = a; *s_out = b;
+  return b > a;
+}
+
+/* Amanatides-Woo traversal over 4 axes (axis resolution R, R, R, F). */
+static int ray4_dda(const uint8_t* g, int32_t R, int32_t F, const double* o, const double* d) {
+  double s_in, s_out;
+  if (!ray4_clip(o, d, &s_in, &s_out)) return 0;
+  int idx[4], step[4];
+  double tmax[4];
+  for (int j = 0; j < 4; ++j) {
+    const int Rj = res4(R, F, j);
+    double p = o[j] + s_in * d[j];
+    double pr = p * (double)Rj;
+    int64_t i = (int64_t)floor(pr);
+    if ((double)i == pr && d[j] < 0.0) i -= 1; /* on a face, moving down */
+    if (i < 0) i = 0;
+    if (i > Rj - 1) i = Rj - 1;
+    idx[j] = (int)i;
+    if (d[j] > 0.0) {
+      step[j] = 1;
+      tmax[j] = ((double)(idx[j] + 1) / (double)Rj - o[j]) / d[j];
+    } else if (d[j] < 0.0) {
+      step[j] = -1;
+      tmax[j] = ((double)idx[j] / (double)Rj - o[j]) / d[j];
+    } else {
+      step[j] = 0;
+      tmax[j] = INFINITY;
+    }
+  }
+  double s = s_in;
+  for (;;) {
+    int a = 0;
+    for (int j = 1; j < 4; ++j)
+      if (tmax[j] < tmax[a]) a = j;
+    double s_next = tmax[a] < s_out ? tmax[a] : s_out;
+    if (s_next > s && occ4(g, R, idx)) return 1;
+    if (tmax[a] >= s_out) return 0;
+    s = s_next;
+    idx[a] += step[a];
+    const int Ra = res4(R, F, a);
+    if (idx[a] < 0 || idx[a] >= Ra) return 0;
+    tmax[a] = (step[a] > 0 ? ((double)(idx[a] + 1) / (double)Ra - o[a])
+                           : ((double)idx[a] / (double)Ra - o[a])) / d[a];
+  }
+}
+
+/* Brute force: slab test of the ray against every occupied cell. */
+static int ray4_brute(const uint8_t* g, int32_t R, int32_t F, const double* o, const double* d) {
+  double s_in, s_out;
+  if (!ray4_clip(o, d, &s_in, &s_out)) return 0;
+  int c[4];
+  for (c[3] = 0; c[3] < F; ++c[3])
+    for (c[0] = 0; c[0] < R; ++c[0])
+      for (c[1] = 0; c[1] < R; ++c[1])
+        for (c[2] = 0; c[2] < R; ++c[2]) {
+          if (!occ4(g, R, c)) continue;
+          double a = s_in, b = s_out;
+          int ok = 1;
+          for (int ax = 0; ax < 4 && ok; ++ax) {
+            const int Ra = res4(R, F, ax);
+            double lo = (double)c[ax] / (double)Ra, hi = (double)(c[ax] + 1) / (double)Ra;
+            if (d[ax] == 0.0) { /* constant coordinate: its half-open cell (R15) */
+              if (cell_index(o[ax], Ra) != c[ax]) ok = 0;
+              continue;
+            }
+            double t0 = (lo - o[ax]) / d[ax], t1 = (hi - o[ax]) / d[ax];
+            if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+            if (t0 > a) a = t0;
+            if (t1 < b) b = t1;
+          }
+          if (ok && b > a) return 1;
+        }
+  return 0;
+}
+
+static int box4_cells(const double* lo, const double* hi, int32_t R, int32_t F, int* a, int* b) {
+  for (int j = 0; j < 4; ++j) {
+    double l = lo[j] < 0.0 ? 0.0 : lo[j];
+    double h = hi[j] > 1.0 ? 1.0 : hi[j];
+    if (!(h >= l)) return 0;
+    a[j] = cell_index(l, res4(R, F, j));
+    b[j] = cell_index(h, res4(R, F, j));
+  }
+  return 1;
+}
+
+/* 4D summed-area table S[(F+1)][(R+1)^3] over (t, x, y, z): S[f][i][j][k] =
+ * number of occupied cells with t-cell < f, x-cell < i, y-cell < j, z-cell < k,
+ * built one axis at a time (prefix sums along x, y, z, then t).          */
+static int32_t* sat4_build(const uint8_t* g, int32_t R, int32_t F) {
+  const int64_t R1 = R + 1, F1 = F + 1;
+  int32_t* S = (int32_t*)calloc((size_t)(F1 * R1 * R1 * R1), sizeof(int32_t));
+#define S4(f, i, j, k) S[(((int64_t)(f) * R1 + (i)) * R1 + (j)) * R1 + (k)]
+  for (int f = 1; f <= F; ++f)
+    for (int i = 1; i <= R; ++i)
+      for (int j = 1; j <= R; ++j)
+        for (int k = 1; k <= R; ++k) {
+          const int c[4] = {i - 1, j - 1, k - 1, f - 1};
+          S4(f, i, j, k) = occ4(g, R, c);
+        }
+  for (int f = 1; f <= F; ++f) /* prefix along z, y, x within each frame */
+    for (int i = 1; i <= R; ++i)
+      for (int j = 1; j <= R; ++j)
+        for (int k = 1; k <= R; ++k) S4(f, i, j, k) += S4(f, i, j, k - 1);
+  for (int f = 1; f <= F; ++f)
+    for (int i = 1; i <= R; ++i)
+      for (int j = 1; j <= R; ++j)
+        for (int k = 1; k <= R; ++k) S4(f, i, j, k) += S4(f, i, j - 1, k);
+  for (int f = 1; f <= F; ++f)
+    for (int i = 1; i <= R; ++i)
+      for (int j = 1; j <= R; ++j)
+        for (int k = 1; k <= R; ++k) S4(f, i, j, k) += S4(f, i - 1, j, k);
+  for (int f = 1; f <= F; ++f) /* then along t */
+    for (int i = 1; i <= R; ++i)
+      for (int j = 1; j <= R; ++j)
+        for (int k = 1; k <= R; ++k) S4(f, i, j, k) += S4(f - 1, i, j, k);
+#undef S4
+  return S;
+}
+
+/* Inclusion-exclusion over the 16 corners of [a, b] (cells inclusive). */
+static int box4_sat(const int32_t* S, int32_t R, int32_t F, const double* lo, const double* hi) {
+  int a[4], b[4];
+  if (!box4_cells(lo, hi, R, F, a, b)) return 0;
+  const int64_t R1 = R + 1;
+  int64_t cnt = 0;
+  for (int c = 0; c < 16; ++c) {
+    int idx[4], sign = 1;
+    for (int ax = 0; ax < 4; ++ax) {
+      if ((c >> ax) & 1) idx[ax] = b[ax] + 1;
+      else { idx[ax] = a[ax]; sign = -sign; }
+    }
+    cnt += sign * (int64_t)S[(((int64_t)idx[3] * R1 + idx[0]) * R1 + idx[1]) * R1 + idx[2]];
+  }
+  return cnt > 0;
+}
+
+static int box4_scan(const uint8_t* g, int32_t R, int32_t F, const double* lo, const double* hi) {
+  int a[4], b[4], c[4];
+  if (!box4_cells(lo, hi, R, F, a, b)) return 0;
+  for (c[3] = a[3]; c[3] <= b[3]; ++c[3])
+    for (c[0] = a[0]; c[0] <= b[0]; ++c[0])
+      for (c[1] = a[1]; c[1] <= b[1]; ++c[1])
+        for (c[2] = a[2]; c[2] <= b[2]; ++c[2])
+          if (occ4(g, R, c)) return 1;
+  return 0;
+}
+
+/* Hyperplane n.(x - p0) = 0 against the closed 4D cell boxes at subdivision
+ * `sub` (1: the cells themselves; 2: each cell split in 2^4 children, an
+ * independent evaluation of the same predicate by convexity).            */
+static int plane4_scan_res(const uint8_t* g, int32_t R, int32_t F, int sub, const double* p0,
+                           const double* nrm) {
+  int c[4];
+  for (c[3] = 0; c[3] < F * sub; ++c[3])
+    for (c[0] = 0; c[0] < R * sub; ++c[0])
+      for (c[1] = 0; c[1] < R * sub; ++c[1])
+        for (c[2] = 0; c[2] < R * sub; ++c[2]) {
+          const int pc[4] = {c[0] / sub, c[1] / sub, c[2] / sub, c[3] / sub};
+          if (!occ4(g, R, pc)) continue;
+          int neg = 0, pos = 0;
+          for (int k = 0; k < 16; ++k) {
+            double s = 0.0;
+            for (int ax = 0; ax < 4; ++ax) {
+              const double x = (double)(c[ax] + ((k >> ax) & 1)) / ((double)res4(R, F, ax) * sub) - p0[ax];
+              s += nrm[ax] * x;
+            }
+            if (s <= 0.0) neg = 1;
+            if (s >= 0.0) pos = 1;
+          }
+          if (neg && pos) return 1;
+        }
+  return 0;
+}
+
 static int label_one(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames, int32_t kind,
                      const float* r, const int32_t* S, int brute) {
   double v[8];
   int nf = (kind == ORA_POINT) ? sd : 2 * sd;
   for (int j = 0; j < nf; ++j) v[j] = (double)r[j];
+  if (sd == 4 && kind != ORA_POINT) {
+    switch (kind) {
+      case ORA_RAY: return brute ? ray4_brute(grid, R, frames, v, v + 4) : ray4_dda(grid, R, frames, v, v + 4);
+      case ORA_BOX: return brute ? box4_scan(grid, R, frames, v, v + 4) : box4_sat(S, R, frames, v, v + 4);
+      case ORA_PLANE: return plane4_scan_res(grid, R, frames, brute ? 2 : 1, v, v + 4);
+    }
+    return 0;
+  }
   if (sd == 2 && kind != ORA_POINT) {
     switch (kind) {
       case ORA_RAY: return brute ? ray2_brute(grid, R, v, v + 2) : ray2_dda(grid, R, v, v + 2);
@@ -395,10 +605,12 @@ static int label_one(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames,
 static int label_impl(const uint8_t* grid, int32_t sd, int32_t R, int32_t frames, int32_t kind,
                       const float* q, int64_t n, uint8_t* y, int brute) {
   if (kind == ORA_POINT && !(sd >= 2 && sd <= 4)) return -1;
-  if (kind != ORA_POINT && sd != 3 && sd != 2) return -1;
+  if (kind != ORA_POINT && !(sd >= 2 && sd <= 4)) return -1;
   int nf = (kind == ORA_POINT) ? sd : 2 * sd;
   int32_t* S = NULL;
-  if (kind == ORA_BOX && !brute && sd == 3) {
+  if (kind == ORA_BOX && !brute && sd == 4) {
+    S = sat4_build(grid, R, frames);
+  } else if (kind == ORA_BOX && !brute && sd == 3) {
     S = (int32_t*)malloc(sizeof(int32_t) * (size_t)(R + 1) * (R + 1) * (R + 1));
     ora_sat_build(grid, R, S);
   } else if (kind == ORA_BOX && !brute) {

@@ -45,7 +45,8 @@ typedef struct { double loss; uint64_t tp, fp, fn, tn; } ora_stats;
  * layout is [frames][R][R][R] and t selects the frame (R15).              */
 int  ora_indicator(const uint8_t* grid, int32_t space_dim, int32_t R, int32_t frames,
                    const double* x);
-/* Exact labels y = g(r) for n records (R16-R19).  Returns 0 or -1 (bad arg). */
+/* Exact labels y = g(r) for n records (R16-R19; 4D rays, hyperplanes and
+ * boxes over the [frames][R][R][R] space-time cells, R48).  Returns 0 or -1. */
 int  ora_label(const uint8_t* grid, int32_t space_dim, int32_t R, int32_t frames,
                int32_t kind, const float* q, int64_t n, uint8_t* y);
 /* Independent brute-force labellers used only to pin ora_label. */
