@@ -16,7 +16,8 @@
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *  - Query records are fp32, row-major [n][nb_record_floats(kind, dim)]:
  *      point: x (n floats; 4D is (x, y, z, t));  ray: (origin, unit direction);
- *      plane: (p0, unit normal);  box: (min corner, max corner).
+ *      plane: (p0, unit normal);  box: (min corner, max corner);
+ *      4D records carry 4 + 4 floats (Suppl. Tab. 4/5 "4D Ray, Plane, Box").
  *  - Labels y are uint8 in {0, 1}, one per record.
  *  - Alignment: device q and y passed to nb_forward, nb_calibrate*,
  *    nb_score, nb_score_async, nb_train_step and nb_hier_score must be
@@ -90,7 +91,9 @@ typedef enum { NB_RELU = 0, NB_SINE = 1 } nb_activation;
  * activation / pe_depth mean ReLU without encoding. */
 typedef struct {
   int32_t kind;          /* nb_query_kind                                    */
-  int32_t space_dim;     /* 2, 3 or 4 (4 = 3D + time, points only)          */
+  int32_t space_dim;     /* 2, 3 or 4 (4 = 3D + time; 4D rays / planes /
+                            boxes are 8-float records over (x, y, z, t), R48;
+                            bf16: widths 32..128, layer 1 K = 32)             */
   int32_t width;         /* hidden width w                                   */
   int32_t hidden_layers; /* L >= 1                                           */
   int32_t n_heads;       /* 0..2 early-exit heads                            */
@@ -286,7 +289,9 @@ nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uin
 void      nb_grid_destroy(nb_grid* g);
 /* y[i] = g(record i) exactly: point lookup, fp64 DDA for rays, SAT for boxes,
  * fp64 voxel-corner cut test for planes (R15-R17, R19; g = any f
- * over the region).  Rays, planes (lines) and boxes: 2D and 3D grids. */
+ * over the region).  Rays, planes (lines) and boxes: 2D and 3D grids
+ * (4D rays / planes / boxes: NB_E_UNSUPPORTED, the tests label them with
+ * the oracle).                                                             */
 nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
                    void* stream);
 

@@ -39,7 +39,6 @@ static bool desc_valid(const nb_desc* d, int* d0_out) {
   if (!d) return false;
   if (d->kind < NB_POINT || d->kind > NB_BOX) return false;
   if (d->space_dim < 2 || d->space_dim > 4) return false;
-  if (d->space_dim == 4 && d->kind != NB_POINT) return false;
   if (d->width < 1 || d->width > 256) return false;
   if (d->hidden_layers < 1 || d->hidden_layers > kMaxLayers) return false;
   if (d->n_heads < 0 || d->n_heads > 2) return false;
@@ -229,7 +228,6 @@ extern "C" {
 
 int64_t nb_record_floats(int32_t kind, int32_t space_dim) {
   if (kind < NB_POINT || kind > NB_BOX || space_dim < 2 || space_dim > 4) return -1;
-  if (space_dim == 4 && kind != NB_POINT) return -1;
   return kind == NB_POINT ? space_dim : 2 * space_dim;
 }
 

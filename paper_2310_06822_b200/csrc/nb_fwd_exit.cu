@@ -499,6 +499,7 @@ void plan_weights(const nb_model* m, ExitParams& p, int lb, int seg, int head) {
 bool exit_compaction_supported(const nb_model* m) {
   const nb_desc& d = m->d;
   return d.precision == NB_BF16 && d.width == kXW && m->pl.pairs == 1 && m->pl.bias_l0 != 0 &&
+         m->pl.k_of[0] == (uint32_t)kEncK &&
          d.activation == NB_RELU && d.pe_depth == 0 &&
          d.n_heads == 2 && d.head_after[0] == 2 && d.head_after[1] == 4 && d.hidden_layers == 6 &&
          m->num_sms * kXSlots <= kMaxRegions;

@@ -403,9 +403,9 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         const uint32_t a = tmem + a_col(s);
         if (l == 0) {
           mma_ts(d, a, dtab[0], idesc, 0u);
-          if (EXT)  // positional encoding: K0 = 32 .. 64
-            for (uint32_t kk = 1; kk < (uint32_t)p.k0 / 16u; ++kk)
-              mma_ts(d, a + kk * 8u, dtab[0] + (uint64_t)(kk * 16u), idesc, 1u);
+          // positional encoding (K0 = 32 .. 64) or 8-float records (K0 = 32)
+          for (uint32_t kk = 1; kk < (uint32_t)p.k0 / 16u; ++kk)
+            mma_ts(d, a + kk * 8u, dtab[0] + (uint64_t)(kk * 16u), idesc, 1u);
         } else {
           if (BF)  // bias first: D = ones * [hi mid lo]^T, then D += A W^T
             mma_ts(d, tmem + kOnesCol, dtab[kMaxLayers + l], idesc, 0u);
@@ -472,6 +472,20 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
         uint32_t c[8];
         encode_cols<D0C, BF>(x, d0, c);
         tmem_st8(trow + a_col(s), c);
+        if (!D0C && p.k0 > kEncK) {  // 8-float records (4D rays / planes / boxes, R48): K = 32,
+          uint32_t c2[8];            // the bias ones at k = 2 d0 .. 2 d0 + 2 land in the second block
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int k = kEncK + 2 * cc + h2;
+              if (BF && k >= 2 * d0 && k < 2 * d0 + 3) v |= 0x3F80u << (16 * h2);
+            }
+            c2[cc] = v;
+          }
+          tmem_st8(trow + a_col(s) + 8u, c2);
+        }
         if (MODE == kTrain) {  // layer-1 input image for the dW GEMM (ReLU, no PE)
           uint8_t* base = p.a.tr.x_img + t * img_tile_bytes(16);
 #pragma unroll

@@ -909,7 +909,9 @@ static cudaError_t launch_tc2p_l(const nb_model* m, int mode, const FwdArgs& a, 
 }
 
 bool tc2_supported(const nb_desc& d) {
-  return d.precision == NB_BF16 && d.width == 256 && d.hidden_layers >= 1 &&
+  // layer 1 is one K = 16 step on CTA pairs: records of up to 6 floats
+  const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
+  return d.precision == NB_BF16 && d.width == 256 && d.hidden_layers >= 1 && enc_k(r) <= kEncK &&
          d.hidden_layers <= kMaxLayers && d.activation == NB_RELU && d.pe_depth == 0;
 }
 

@@ -1075,3 +1075,90 @@ def test_misaligned_views_rejected_aligned_offsets_work():
     assert m.score(qd[16:], yd[16:]) == m.score(qd[16:].clone(), yd[16:].clone())
     assert torch.equal(m.forward(qd[16:]), m.forward(qd[16:].clone()))
     torch.cuda.synchronize()   # the context is healthy
+
+
+# ---------------------------------------------------------------- NEXT-3: 4D rays, hyperplanes, boxes (R48)
+@pytest.mark.parametrize("kind,n", [("ray", (1 << 15) + 77), ("box", (1 << 15) + 5), ("plane", (1 << 13) + 3)])
+def test_4d_queries_bf16_forward_counts_and_gradient(kind, n):
+    """8-float records through the tensor-core kernels (layer 1 K = 32: hi, lo
+    and the bias ones in a second K step): encoder bytes bit-exact, sigmoid
+    within 2e-2 of fp64, counts equal to the bf16-emulating oracle outside
+    the band, FN = 0 after calibration on both sides, and one training
+    step's per-tensor gradient within 2e-2 of the kernel-precision oracle."""
+    cfg = nbgen.EXTRA_CONFIGS["c4" + kind]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    assert 0.01 < y.mean() < 0.99
+    a = oracle.arch_of(cfg)
+    th = scaled_params(cfg, 13, scale=1.8)
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(th)
+    qd, yd = cuda(q), cuda(y)
+    assert np.array_equal(m.encode(qd).cpu().numpy().view(np.uint16), oracle.encode_bf16(q.numpy()))
+    z = m.forward(qd).cpu().double().numpy()
+    zr = oracle.forward(a, th.double().numpy(), q.numpy())
+    assert np.abs(sigmoid(z) - sigmoid(zr)).max() <= 2e-2
+    tau = m.calibrate(qd, yd).numpy()
+    c = m.score(qd, yd)
+    assert c["fn"] == 0 and c["tp"] == int(y.sum())
+    ze = oracle.forward(a, th.double().numpy(), q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    assert oracle.score(ze, y, te)["fn"] == 0
+    keep = ~band_mask(z, tau, ze, te)
+    assert keep.mean() > 0.95
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    assert all(cg[k] == co[k] for k in ("tp", "fp", "fn", "tn")), (cg, co)
+    nt = 4096 + 33
+    st = m.train_step(qd[:nt], yd[:nt], alpha=40.0, stats=True)
+    g = m.get_grad().double().numpy()
+    le, ge, _ = oracle.loss_grad(a, th.double().numpy(), q.numpy()[:nt], y[:nt], 40.0, 1.0, mode=oracle.BF16_EMU)
+    assert abs(st["loss"] - le) <= 1e-3 * abs(le)
+    rel = {nm: np.linalg.norm(g[sl] - ge[sl]) / np.linalg.norm(ge[sl]) for nm, sl in param_tensors(cfg)
+           if np.linalg.norm(ge[sl]) > 0}
+    assert max(rel.values()) <= 2e-2, rel
+
+
+@pytest.mark.parametrize("kind", ["ray", "box", "plane"])
+def test_4d_queries_fp32_path(kind):
+    """fp32 CUDA-core path with 8-float records: forward within 1e-5 of fp64
+    (P1) and the gradient within 1e-4."""
+    cfg = nbgen.EXTRA_CONFIGS["c4" + kind]
+    n = 4096 + 17
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    a = oracle.make_arch(8, 32, 2)
+    th = torch.from_numpy(np.random.default_rng(3).normal(size=oracle.num_params(a)) * 0.3).float()
+    m = nb.Model(nb.Desc(kind, 4, 32, 2, (), "fp32"), DEV)
+    m.set_params(th)
+    z = m.forward(cuda(q)).cpu().double().numpy()
+    zr = oracle.forward(a, th.double().numpy(), q.numpy())
+    assert np.all(np.abs(z - zr) <= 1e-5 * np.maximum(1.0, np.abs(zr)))
+    m.train_step(cuda(q), cuda(y), alpha=9.0)
+    g = m.get_grad().double().numpy()
+    _, gr, _ = oracle.loss_grad(a, th.double().numpy(), q.numpy(), y, 9.0, 1.0)
+    assert np.linalg.norm(g - gr) <= 1e-4 * np.linalg.norm(gr)
+
+
+def test_4d_training_run_conservative():
+    """A short training run on 4D boxes (the c4 scene, 300 steps x 2^14,
+    alpha 1 -> 1000): FN = 0 after calibration and FP below the initial
+    network's."""
+    cfg = nbgen.EXTRA_CONFIGS["c4box"]
+    m = nb.Model(desc_of(cfg), DEV)
+    m.set_params(nbgen.init_params(cfg))
+    qe = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 1 << 16)
+    ye = labels_oracle(cfg, qe.numpy())
+    qd, yd = cuda(qe), cuda(ye)
+    m.calibrate(qd, yd)
+    fp0 = m.score(qd, yd)["fp"]
+    T, B = 300, 1 << 14
+    qt = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, 4 * B)
+    yt = labels_oracle(cfg, qt.numpy())
+    qtd, ytd = cuda(qt), cuda(yt)
+    for t in range(T):
+        sl = slice((t % 4) * B, (t % 4 + 1) * B)
+        m.train_step(qtd[sl], ytd[sl], alpha=nb.alpha(t, T))
+    m.calibrate(qd, yd)
+    c = m.score(qd, yd)
+    assert c["fn"] == 0 and c["fp"] < fp0, (c, fp0)
