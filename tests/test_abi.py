@@ -36,7 +36,8 @@ def test_host_only_calls():
     assert L.nb_record_floats(nb.POINT, 3) == 3
     assert L.nb_record_floats(nb.RAY, 3) == 6
     assert L.nb_record_floats(nb.POINT, 4) == 4
-    assert L.nb_record_floats(nb.RAY, 4) == -1
+    assert L.nb_record_floats(nb.RAY, 4) == 8      # 4D rays: (origin, direction) in (x, y, z, t) (R48)
+    assert L.nb_record_floats(nb.BOX, 5) == -1
     assert nb.Desc("point", 3, 50, 2, precision="fp32").num_params == 2801
     assert nb.Desc("point", 4, 128, 6, (2, 4)).num_params == 83587
     assert nb.alpha(0, 200) == 1.0 and nb.alpha(199, 200) == 1000.0
