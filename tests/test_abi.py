@@ -45,8 +45,9 @@ def test_host_only_calls():
 
 
 def test_invalid_desc_rejected_without_gpu():
-    d = nb.Desc("ray", 4, 64, 4).to_c()
+    d = nb.Desc("ray", 5, 64, 4).to_c()          # no 5D records
     assert nb.lib().nb_num_params(C.byref(d)) == -1
+    assert nb.Desc("ray", 4, 64, 4).num_params == (8 + 1) * 64 + 3 * 65 * 64 + 65  # 4D ray: 8 inputs (R48)
     h = C.c_void_p()
     assert nb.lib().nb_model_create(C.byref(d), 0, C.byref(h)) == 1  # NB_E_ARG
 
