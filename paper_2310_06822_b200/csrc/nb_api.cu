@@ -9,6 +9,7 @@
 #include <cmath>
 #include <string>
 
+#include "nb_device.cuh"
 #include "nb_internal.cuh"
 
 namespace nb {
@@ -173,6 +174,26 @@ static void timing_end(const nb_model* m, cudaStream_t s) {
   cudaEventRecord(mm->ev_pool[2 * mm->ev_used + 1], s);
   mm->ev_used += 1;
   mm->kernel_launches += 1;
+}
+
+// NB_CHECKS self-test (tests/test_gpu_checked.py): a kernel waits on an
+// mbarrier phase that never completes; the checked build must trap with a
+// diagnostic instead of hanging.  Release builds return NB_E_UNSUPPORTED.
+__global__ void k_selftest_lost_arrive() {
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_barrier_init();
+    mbar_wait(smem_u32(&bar), 0u);  // nobody arrives
+  }
+}
+extern "C" int nb_debug_selftest_lost_arrive(void) {
+#ifdef NB_CHECKS
+  k_selftest_lost_arrive<<<1, 32>>>();
+  return (int)cudaDeviceSynchronize();
+#else
+  return NB_E_UNSUPPORTED;
+#endif
 }
 
 // Measurement / test switch: score models with exit heads densely (every head

@@ -165,7 +165,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-#ifdef NB_MBAR_NOHINT
+#if defined(NB_MBAR_NOHINT) || defined(NB_CHECKS)
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
 #else
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, 10000000;\n\t"
@@ -188,13 +188,46 @@ __device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// NB_CHECKS builds (libnb_checked.so, tests/test_gpu_checked.py): the
+// stand-in for compute-sanitizer's synccheck/memcheck on the hand-rolled
+// pipelines.  A wait that has not completed after 2^24 polls (seconds; the
+// checked build polls without a suspend-time hint) is
+// a lost arrive or a phase error: report the barrier and trap instead of
+// hanging; NB_CHECK() traps on a violated invariant (bounds, alignment).
+#ifdef NB_CHECKS
+#define NB_CHECK(cond, ...)                                                          \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("NB_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                              \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define NB_CHECK(cond, ...) \
+  do {                      \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef NB_CHECKS
+  uint64_t polls = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++polls == (1ull << 24)) {
+      printf("NB_CHECK mbarrier timeout: bar 0x%x parity %u block %d thread %d\n", bar, parity,
+             (int)blockIdx.x, (int)threadIdx.x);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA engine).
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {
+  NB_CHECK(((uintptr_t)src & 15u) == 0 && (dst & 15u) == 0 && (bytes & 15u) == 0 && bytes > 0);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
           "r"(dst),

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
   tc_fence_after();
   if (IN_IMG) num_tiles = pref[R];
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   {  // ones block (bias folding): k = 0, 1, 2 of every row are 1.0
     if (warp < 4) {
       const uint32_t ones[8] = {0x3F803F80u, 0x00003F80u, 0u, 0u, 0u, 0u, 0u, 0u};

@@ -174,6 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
   cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   if (BF) {  // ones block of hidden layer l: bf16 1.0 at k = 3 (l - 1) .. 3 (l - 1) + 2
     if (warp < 4) {
       for (int l = 1; l < (LC ? LC : p.L); ++l) {
@@ -225,8 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
     if (warp == 0) {
       if (lane == 0) mbar_arrive_remote_cta(a_full_leader);
       if (leader) {
-        while (!mbar_try_wait_cluster(a_full, aph)) {
-        }
+        mbar_wait(a_full, aph);
         aph ^= 1u;
         tc_fence_after();
         if (elect_one()) {
@@ -566,6 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   mbar_wait(w_bar, 0);
 
   const int64_t n = p.a.n;
@@ -765,6 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
             if (!last) tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
+            NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
             if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
               uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
 #pragma unroll
@@ -811,6 +813,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
         const int yv = ylab[b * kTile + row];
         const int64_t r = half_base(tile) + row;
         const bool valid = r < n;
+        NB_CHECK(!valid || (r >= 0 && r < n));
         if (MODE == kForward) {
           if (valid) {
             p.a.logits[r] = z;

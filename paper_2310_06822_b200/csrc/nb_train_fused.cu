@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256, 1) k_train_fused(const FusedParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   if (warp < 4) {  // forward bias-folding ones block (k = 0, 1, 2 of every row)
     const uint32_t ones[8] = {0x3F803F80u, 0x00003F80u, 0u, 0u, 0u, 0u, 0u, 0u};
     tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + 96u, ones);

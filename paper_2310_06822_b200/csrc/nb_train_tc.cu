@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   mbar_wait(smem_u32(bars), 0);
 
   const int s = warp / WPS, qw = warp & 3, rit = qw * 32 + lane;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   const int64_t per = (num_tiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = min(num_tiles, blockIdx.x * per), t1 = min(num_tiles, t0 + per);
   const int fa_job = min(128, j.fa - j.m_off);

@@ -65,6 +65,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_bwd_tc2(co
   cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   mbar_wait(w_bar, 0);
 
   const int qw = warp & 3, grp = warp >> 2, col0 = grp * CPT;
