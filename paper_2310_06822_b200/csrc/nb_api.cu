@@ -757,10 +757,18 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
     m->train_scratch_bytes = need;
   }
   NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
-  if (tc)
-    NB_CUDA(launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s));
-  else
+  if (tc) {
+    g_err.clear();
+    const cudaError_t e = launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s);
+    if (e != cudaSuccess) {  // keep the failing stage's detail
+      const std::string stage = g_err;
+      cuda_fail(e, "nb_train_step");
+      if (!stage.empty()) g_err += " [" + stage + "]";
+      return NB_E_CUDA;
+    }
+  } else {
     NB_CUDA(launch_train_simt(m, q, y, n_local, n_global, alpha, beta, s));
+  }
   if (m->comm) {
     if (comm_allreduce_f32_sum(m, m->grad, m->P, s)) return NB_E_NCCL;
   }

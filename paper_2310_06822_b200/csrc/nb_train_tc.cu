@@ -590,7 +590,7 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
   a.tr.num_tiles = T;
   const bool pairs = m->pl.pairs == 2;  // w = 256: CTA-pair forward and backward
   cudaError_t e = pairs ? launch_fwd_tc2(m, kTrain, a, st) : launch_fwd_tc(m, kTrain, a, st);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return set_error("training forward: %s", cudaGetErrorString(e)), e;
   // 2. backward chain
   BwdParams bp;
   bp.packed = m->packed;
@@ -612,7 +612,7 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
     e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st);
   else
     e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) return set_error("backward chain: %s", cudaGetErrorString(e)), e;
   // 3. dW GEMMs of every job (one launch)
   js.accumulate = first ? 0 : 1;
   return run_dw(js, T, st);
