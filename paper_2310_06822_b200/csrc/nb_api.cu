@@ -317,6 +317,13 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   m->P = nb_num_params(desc);
   param_offsets(m->d, m->din, &m->po);
   pack_layout(m->d, &m->pl);
+  // CTA-pair kernels keep one pair image (+ ~16 KB of staging, barriers and
+  // ones operands) in shared memory: deeper / PE pair nets do not fit
+  if (m->pl.pairs == 2 && m->pl.bytes + 16u * 1024u > 227u * 1024u) {
+    set_error("w = 256 image of %u bytes exceeds the shared memory of a CTA pair", m->pl.bytes);
+    delete m;
+    return NB_E_UNSUPPORTED;
+  }
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t bytes) {

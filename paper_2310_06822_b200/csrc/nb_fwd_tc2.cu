@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "nb_device.cuh"
+#include "nb_fwd_tc.cuh"  // encode_cols_pe, sin_act (sine / PE pair kernels)
 #include "nb_internal.cuh"
 
 namespace nb {
@@ -25,6 +26,7 @@ struct TcParams2 {
   const uint8_t* packed;  // pl.pairs images
   PackLayout pl;
   int d0, L, nh, ha0, ha1;
+  int act, pe;            // k_fwd_tc2p<EXT>: nb_activation and PE depth (R41, R42)
   int64_t num_pairs;      // 256-row tile pairs
   unsigned long long* trace;  // NB_TRACE builds: timeline of CTA 0 (k_fwd_tc2p)
 };
@@ -495,8 +497,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
 // (g0 + g1 + g2 + g3, each group's a-half then b-half) and classifies /
 // calibrates / writes the logits, off the epilogue's critical path
 // (partials double-buffered by tile parity, xfull / xfree mbarriers).
-// D0: compile-time record width for the encoder (0: run time).
-template <int LC, int MODE, int D0>
+// D0: compile-time record width for the encoder (0: run time).  EXT: the
+// paper's sine activation and NeRF positional encoding (
+// R41, R42; run-time p.act / p.pe, D0 > 0 for PE): sin(z) epilogues and a
+// K = 64 layer-1 operand in the PE layout (4 K-steps).
+template <int LC, int MODE, int D0, bool EXT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(const TcParams2 p) {
   constexpr int W = 256, NEPI = 16, CPT = 32;
   const int L = LC ? LC : p.L;
@@ -592,8 +597,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   const uint32_t idesc = make_idesc_bf16(256, 128);
   const uint32_t a_done_leader = mapa_shared(a_done, 0), b_done_leader = mapa_shared(b_done, 0);
   // B descriptors of layer l, image rows [64 h, 64 h + 64) of this CTA
+  const bool sine = EXT && p.act == NB_SINE;
+  const uint32_t k0steps = p.pl.k_of[0] / 16u;  // layer-1 K-steps (1; 4 with PE)
   auto bdesc = [&](int l, int h) {
-    const uint32_t K = l == 0 ? (uint32_t)kEncK : (uint32_t)W;
+    const uint32_t K = l == 0 ? p.pl.k_of[0] : (uint32_t)W;
     const uint32_t sbo = K / 8u * 128u;
     return make_sdesc(sbase + p.pl.off_w[l] + (uint32_t)h * 8u * sbo, 128u, sbo);
   };
@@ -630,9 +637,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
     if (i >= 2) mbar_wait(xfree(b), (uint32_t)((i >> 1) - 1) & 1u);
     ylab[b * kTile + rit] = (uint8_t)yv;
     uint32_t c[8];
-    if (bias0) encode_cols2<true>(x, d0, c);
-    else encode_cols2<false>(x, d0, c);
-    tmem_st8(trow + acol(abuf), c);
+    if (EXT && D0 > 0 && p.pe > 0) {  // positional encoding: K = 64 PE operand layout (R42)
+      uint32_t cp[32];
+      encode_cols_pe<(D0 > 0 ? D0 : 1)>(x, p.pe, cp);
+#pragma unroll
+      for (int g4 = 0; g4 < 4; ++g4)
+        tmem_st8(trow + acol(abuf) + 8u * (uint32_t)g4, *reinterpret_cast<const uint32_t(*)[8]>(cp + 8 * g4));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = cp[j];
+    } else {
+      if (bias0) encode_cols2<true>(x, d0, c);
+      else encode_cols2<false>(x, d0, c);
+      tmem_st8(trow + acol(abuf), c);
+    }
     if (MODE == kTrain && 2 * t + rank < p.a.tr.num_tiles) {  // layer-1 input image (dW GEMM)
       uint8_t* base = p.a.tr.x_img + (2 * t + rank) * img_tile_bytes(16);
 #pragma unroll
@@ -673,7 +690,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
         const uint32_t A = tmem + acol(ab);
         if (elect_one()) {
           if (ln == 0) {
-            mma_ts2(tmem, A, bdesc(0, 0), idesc, 0u);
+            for (uint32_t kk = 0; kk < k0steps; ++kk)
+              mma_ts2(tmem, A + kk * 8u, bdesc(0, 0) + (uint64_t)(kk * 16u), idesc, kk > 0 ? 1u : 0u);
             mma_commit2(acc_a);
           } else {
             const uint64_t bd = bdesc(ln, 0);
@@ -693,7 +711,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
         tc_fence_after();
         if (elect_one()) {
           if (ln == 0) {
-            mma_ts2(tmem + 128u, A, bdesc(0, 1), idesc, 0u);
+            for (uint32_t kk = 0; kk < k0steps; ++kk)
+              mma_ts2(tmem + 128u, A + kk * 8u, bdesc(0, 1) + (uint64_t)(kk * 16u), idesc, kk > 0 ? 1u : 0u);
             mma_commit2(acc_b);
           } else {
             const uint64_t bd = bdesc(ln, 0), bd1 = bdesc(ln, 1);
@@ -763,8 +782,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
           }
           if (!last || MODE == kTrain) {
             uint32_t pk[16];
+            if (sine) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+              for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(sin_act(t[2 * j]), sin_act(t[2 * j + 1]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
+            }
             if (!last) tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
             NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
             if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
@@ -777,9 +801,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
           }
           if (last) {
             const float* wo = wout + f0;
+            if (sine) {
 #pragma unroll
-            for (int i = 0; i < CPT; i += 2)
-              fma2p(zp, zq, relu_nan(t[i]), relu_nan(t[i + 1]), wo[i], wo[i + 1]);
+              for (int i = 0; i < CPT; i += 2) fma2p(zp, zq, sin_act(t[i]), sin_act(t[i + 1]), wo[i], wo[i + 1]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < CPT; i += 2)
+                fma2p(zp, zq, relu_nan(t[i]), relu_nan(t[i + 1]), wo[i], wo[i + 1]);
+            }
             if (h == 0 && g == 0 && has_next) encode(next, i_tile + 1, (s + 1) & 1u);
             if (h == 1) {  // this group's partial of the output logit -> the classifier
               xch[((i_tile & 1) * 4 + g) * 128 + rit] = zp + zq;
@@ -876,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   if (MODE == kScore && warp == 1 && p.a.ticket) finalize_counts(p.a);
 }
 
-template <int LC, int MODE, int D0>
+template <int LC, int MODE, int D0, bool EXT = false>
 static cudaError_t launch_tc2p_m(const nb_model* m, const FwdArgs& a, cudaStream_t st) {
   TcParams2 p;
   p.a = a;
@@ -886,6 +915,8 @@ static cudaError_t launch_tc2p_m(const nb_model* m, const FwdArgs& a, cudaStream
   p.L = m->d.hidden_layers;
   p.nh = 0;
   p.ha0 = p.ha1 = 0;
+  p.act = m->d.activation;
+  p.pe = m->d.pe_depth;
 #ifdef NB_TRACE
   p.trace = g_trace_buffer;
 #else
@@ -895,12 +926,21 @@ static cudaError_t launch_tc2p_m(const nb_model* m, const FwdArgs& a, cudaStream
   if (p.num_pairs == 0) return cudaSuccess;
   const size_t smem = ((m->pl.bytes + 15) & ~15u) + 8 * 12 + 16 + sizeof(float) * 2 * 4 * 128 + 4 * 16 +
                       sizeof(float) * 2 * kTile * 8 + 4 * kTile + 128 + 256 * kMaxLayers;
-  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc2p<LC, MODE, D0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc2p<LC, MODE, D0, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const int pairs = (int)std::min<int64_t>(p.num_pairs, m->num_sms / 2);
-  k_fwd_tc2p<LC, MODE, D0><<<2 * pairs, 576, smem, st>>>(p);
+  k_fwd_tc2p<LC, MODE, D0, EXT><<<2 * pairs, 576, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+// sine / PE pair kernels (forward, calibrate, score; generic layer count)
+template <int D0>
+static cudaError_t launch_tc2p_ext(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (mode == kForward) return launch_tc2p_m<0, kForward, D0, true>(m, a, st);
+  if (mode == kCalibrate) return launch_tc2p_m<0, kCalibrate, D0, true>(m, a, st);
+  if (mode == kScore) return launch_tc2p_m<0, kScore, D0, true>(m, a, st);
+  return cudaErrorInvalidValue;  // training of sine / PE pair nets: not built (nb_train_step refuses)
 }
 
 template <int LC, int D0>
@@ -914,8 +954,12 @@ static cudaError_t launch_tc2p_l(const nb_model* m, int mode, const FwdArgs& a, 
 bool tc2_supported(const nb_desc& d) {
   // layer 1 is one K = 16 step on CTA pairs: records of up to 6 floats
   const int r = d.kind == NB_POINT ? d.space_dim : 2 * d.space_dim;
-  return d.precision == NB_BF16 && d.width == 256 && d.hidden_layers >= 1 && enc_k(r) <= kEncK &&
-         d.hidden_layers <= kMaxLayers && d.activation == NB_RELU && d.pe_depth == 0;
+  if (d.precision != NB_BF16 || d.width != 256 || d.hidden_layers < 1 || d.hidden_layers > kMaxLayers)
+    return false;
+  if (d.activation != NB_RELU || d.pe_depth > 0)  // sine / PE pairs: no exit heads; PE of 2D / 3D points
+    return d.n_heads == 0 && (d.pe_depth == 0 ? enc_k(r) <= kEncK
+                                              : (r == 2 || r == 3) && r * (1 + d.pe_depth) + 3 <= 32);
+  return enc_k(r) <= kEncK;
 }
 
 template <int LC, int MODE, bool BF>
@@ -957,6 +1001,12 @@ static bool tc2_single() {
 }
 
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t st) {
+  if (m->d.activation != NB_RELU || m->d.pe_depth > 0) {  // sine / PE (R41, R42)
+    if (m->d.pe_depth == 0) return launch_tc2p_ext<0>(m, mode, a, st);
+    if (m->d0 == 2) return launch_tc2p_ext<2>(m, mode, a, st);
+    if (m->d0 == 3) return launch_tc2p_ext<3>(m, mode, a, st);
+    return cudaErrorInvalidValue;
+  }
   if (m->d.n_heads == 0 && !tc2_single()) {  // pipelined halves
     if (m->d.hidden_layers == 4 && m->d0 == 6) return launch_tc2p_l<4, 6>(m, mode, a, st);  // BJ configs[4]
     return launch_tc2p_l<0, 0>(m, mode, a, st);

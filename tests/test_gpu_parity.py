@@ -750,17 +750,51 @@ def test_bf16_sine_pe_forward_and_counts(name, width, layers, pe, n):
 
 
 def test_sine_pe_unsupported_paths_fail_loudly():
-    """nb_encode with PE (the kernels encode in place) and sine / PE nets on
-    CTA pairs (w = 256) are not built: NB_E_UNSUPPORTED, never a silent
-    fallback."""
+    """Paths not built fail loudly (NB_E_UNSUPPORTED, never a silent
+    fallback): nb_encode with PE (the kernels encode in place), training of
+    sine / PE nets on CTA pairs (w = 256), sine pair nets with exit heads."""
     cfg, desc, a, q, y, th = _sine_case("c2", 64, 3, 2, "bf16", 1024)
     m = nb.Model(desc, DEV)
     m.set_params(torch.from_numpy(th).float())
     with pytest.raises(nb.NBError) as ei:
         m.encode(cuda(q))
     assert "UNSUPPORTED" in str(ei.value)
+    m2 = nb.Model(nb.Desc("point", 3, 256, 3, (), "bf16", activation="sine"), DEV)
+    with pytest.raises(nb.NBError) as ei:
+        m2.train_step(cuda(q), cuda(y), alpha=2.0)
+    assert "UNSUPPORTED" in str(ei.value)
     with pytest.raises(nb.NBError):
-        nb.Model(nb.Desc("point", 3, 256, 3, (), "bf16", activation="sine"), DEV)
+        nb.Model(nb.Desc("point", 3, 256, 4, (2,), "bf16", activation="sine"), DEV)
+    with pytest.raises(nb.NBError) as ei:   # a 4-layer PE pair image exceeds shared memory
+        nb.Model(nb.Desc("point", 3, 256, 4, (), "bf16", activation="sine", pe_depth=4), DEV)
+    assert "UNSUPPORTED" in str(ei.value)
+
+
+@pytest.mark.parametrize("name,layers,pe,n", [("c2", 3, 0, 256 * 74 * 2 + 77), ("c1", 3, 8, 256 * 74 * 2 + 5),
+                                              ("c2", 3, 4, 256 * 74 + 3), ("c2", 4, 0, 256 * 74 * 3 + 11)])
+def test_bf16_sine_pe_on_cta_pairs(name, layers, pe, n):
+    """The paper's architecture at w = 256 (sine hidden layers; NeRF
+    encoding) on the pipelined CTA-pair kernel: sigmoid within
+    2e-2 of fp64, counts equal to the bf16-emulating oracle outside the band,
+    FN = 0 after calibration."""
+    cfg, desc, a, q, y, th = _sine_case(name, 256, layers, pe, "bf16", n, scale=0.7)
+    m = nb.Model(desc, DEV)
+    m.set_params(torch.from_numpy(th).float())
+    th32 = torch.from_numpy(th).float().double().numpy()
+    qd, yd = cuda(q), cuda(y)
+    z, p = m.forward(qd, prob=True)
+    zr = oracle.forward(a, th32, q.numpy())[:, 0]
+    assert np.max(np.abs(p.cpu().double().numpy() - 1 / (1 + np.exp(-zr)))) <= 2e-2
+    tau = m.calibrate(qd, yd).numpy()
+    assert m.score(qd, yd)["fn"] == 0
+    ze = oracle.forward(a, th32, q.numpy(), oracle.BF16_EMU)
+    te, _ = oracle.calibrate(ze, y)
+    zg = z.cpu().double().numpy()
+    keep = ~band_mask(zg, tau, ze, te)
+    assert keep.mean() > 0.9
+    cg = m.score(cuda(q.numpy()[keep]), cuda(y[keep]))
+    co = oracle.score(ze[keep], y[keep], te)
+    assert all(cg[k] == co[k] for k in ("tp", "fp", "fn", "tn")), (cg, co)
 
 
 def _tensor_slices(din, width, layers):
