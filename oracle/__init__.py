@@ -69,6 +69,7 @@ def lib():
             "ora_label_brute": (C.c_int, [P, I32, I32, I32, I32, P, I64, P]),
             "ora_sat_build": (None, [P, I32, P]),
             "ora_encode_bf16": (None, [P, I64, I32, P]),
+            "ora_encode_pe": (None, [P, I64, I32, I32, P]),
             "ora_bf16_rne": (C.c_uint16, [C.c_float]),
             "ora_num_params": (I64, [P]),
             "ora_forward": (None, [P, P, P, I64, I32, P]),
@@ -160,6 +161,15 @@ def encode_bf16(q) -> np.ndarray:
     n, d0 = q.shape
     out = np.zeros((n, 16), np.uint16)
     lib().ora_encode_bf16(_ptr(q), n, d0, _ptr(out))
+    return out
+
+
+def encode_pe(q, pe) -> np.ndarray:
+    """bf16 PE operand [n][64] (R42): hi at [0, d_in), lo at [32, 32 + d_in)."""
+    q = _np(q, np.float32)
+    n, d0 = q.shape
+    out = np.zeros((n, 64), np.uint16)
+    lib().ora_encode_pe(_ptr(q), n, d0, pe, _ptr(out))
     return out
 
 

@@ -689,6 +689,29 @@ static void positional_encoding(const ora_arch* a, const float* r, double* f) {
 
 /* Hidden activation sigma and its derivative: ReLU (R1, R25: ReLU'(0) = 0) or
  * sine with frequency 1 ("Sinusoidal activations"; R41).            */
+/* The K = 64 bf16 operand of a PE net (R42, R20): each fp64 feature of
+ * gamma(x) rounded to fp32, then split into the bf16 pair hi = RNE(f),
+ * lo = RNE(f - hi); hi at [0, d_in), lo at [32, 32 + d_in), zeros elsewhere. */
+void ora_encode_pe(const float* q, int64_t n, int32_t d0, int32_t pe, uint16_t* out) {
+  ora_arch a;
+  memset(&a, 0, sizeof(a));
+  a.d0 = d0;
+  a.pe = pe;
+  const int din = input_dim(&a);
+  double f[64];
+  for (int64_t i = 0; i < n; ++i) {
+    uint16_t* o = out + i * 64;
+    for (int j = 0; j < 64; ++j) o[j] = 0;
+    positional_encoding(&a, q + i * d0, f);
+    for (int j = 0; j < din && j < 32; ++j) {
+      const float x = (float)f[j];
+      const uint16_t hi = ora_bf16_rne(x);
+      o[j] = hi;
+      o[32 + j] = ora_bf16_rne(x - bf16_to_f(hi));
+    }
+  }
+}
+
 static double act_fn(const ora_arch* a, double z) { return a->act ? sin(z) : (z > 0.0 ? z : 0.0); }
 static double act_grad(const ora_arch* a, double z) { return a->act ? cos(z) : (z > 0.0 ? 1.0 : 0.0); }
 

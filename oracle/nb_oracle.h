@@ -59,6 +59,9 @@ void ora_sat_build(const uint8_t* grid, int32_t R, int32_t* S);
 /* bf16 hi/lo split: out[i][0..d0) = RNE_bf16(x), out[i][d0..2d0) = RNE_bf16(x - hi),
  * zero padded to 16 (bf16 bit patterns).                                   */
 void ora_encode_bf16(const float* q, int64_t n, int32_t d0, uint16_t* out);
+/* Positional-encoding operand (R42): fp64 gamma(x) -> fp32 -> bf16 (hi, lo),
+ * hi at [0, d_in), lo at [32, 32 + d_in) of 64 columns per record.         */
+void ora_encode_pe(const float* q, int64_t n, int32_t d0, int32_t pe, uint16_t* out);
 uint16_t ora_bf16_rne(float x);
 
 /* ---- MLP h_theta (§3.4; Suppl. Tab. 4) -------------------------- */

@@ -149,3 +149,25 @@ def test_sine_grad_central_finite_differences():
         tm[i] -= h
         fd[i] = (oracle.loss_grad(a, tp, q, y, 5.0, 1.0)[0] - oracle.loss_grad(a, tm, q, y, 5.0, 1.0)[0]) / (2 * h)
     assert np.allclose(fd, g, rtol=1e-6, atol=1e-9 * np.abs(g).max())
+
+
+def test_encode_pe_operand_layout_and_values():
+    """oracle.encode_pe (the K = 64 bf16 PE operand, R42/R20): hi at
+    [0, d_in), lo at [32, 32 + d_in), zeros elsewhere; hi + lo reproduces the
+    written-out features gamma(x) (x, then sin / cos of 2^k pi x per
+    frequency) to the fp32 rounding, and hi is the RNE bf16 of that fp32."""
+    import torch
+    q = np.random.default_rng(1).random((200, 2)).astype(np.float32)
+    e = oracle.encode_pe(q, 8)
+    assert e.shape == (200, 64) and not e[:, 18:32].any() and not e[:, 50:].any()
+    tof = lambda u: torch.from_numpy(u.view(np.int16).astype(np.int32) << 16).view(torch.float32).numpy()  # noqa: E731
+    v = tof(e[:, :18].copy()).astype(np.float64) + tof(e[:, 32:50].copy())
+    x = q.astype(np.float64)
+    feats = [x[:, 0], x[:, 1]]
+    for k in range(4):
+        feats += [np.sin(2 ** k * np.pi * x[:, 0]), np.sin(2 ** k * np.pi * x[:, 1]),
+                  np.cos(2 ** k * np.pi * x[:, 0]), np.cos(2 ** k * np.pi * x[:, 1])]
+    ref = np.stack(feats, 1)
+    assert np.all(np.abs(v - ref) <= 2.0 ** -16 * np.abs(ref) + 1e-12)
+    hi = torch.from_numpy(ref.astype(np.float32)).bfloat16().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(e[:, :18], hi)
