@@ -174,8 +174,11 @@ nb_status nb_comm_version(int32_t* version);
 /* a1 encoder (R20).  NB_BF16: x_out is uint16 [n][16] bf16 bit
  * patterns (hi(0..d0-1), lo(0..d0-1), zeros); NB_FP32: x_out is fp32 [n][d0]
  * (identity).  The compute calls below encode in-kernel; this exposes the exact
- * layer-1 operand for parity.  Models with pe_depth > 0 return
- * NB_E_UNSUPPORTED (their encoding runs inside the kernels only).            */
+ * layer-1 operand for parity.  NB_BF16 models with pe_depth = L > 0 (R42):
+ * x_out is uint16 [n][64], the K = 64 positional-encoding operand the kernels
+ * build (features gamma(x) in fp32, each split into a bf16 (hi, lo) pair:
+ * hi at [0, d_in), lo at [32, 32 + d_in), zeros elsewhere; d_in = r (1 + L)).
+ * NB_FP32 models with pe_depth > 0 return NB_E_UNSUPPORTED.                */
 nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream);
 
 /* a1-a4: logits[n][1 + n_heads] (output logit z, then head logits e_k), fp32;

@@ -304,7 +304,7 @@ class Model:
     def encode(self, q: torch.Tensor) -> torch.Tensor:
         n = q.shape[0]
         if self.desc.precision == "bf16":
-            out = torch.empty(n, 16, dtype=torch.int16, device=q.device)
+            out = torch.empty(n, 64 if self.desc.pe_depth else 16, dtype=torch.int16, device=q.device)
         else:
             out = torch.empty(n, self.d0, dtype=torch.float32, device=q.device)
         _check(lib().nb_encode(self._h, self._q(q), n, out.data_ptr(), _stream(self.device)), "nb_encode")

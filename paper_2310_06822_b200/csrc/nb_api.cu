@@ -505,11 +505,14 @@ nb_status nb_model_get_thresholds(const nb_model* m, float* tau, int32_t n) {
 
 nb_status nb_encode(const nb_model* m, const float* q, int64_t n, void* x_out, void* stream) {
   if (!m || n < 0 || (n > 0 && (!q || !x_out))) return set_error("bad argument"), NB_E_ARG;
-  if (m->d.pe_depth > 0)  // the kernels encode in place; no materialised PE operand yet
-    return set_error("nb_encode: positional encoding is applied inside the kernels only"),
+  if (m->d.pe_depth > 0 && m->d.precision != NB_BF16)
+    return set_error("nb_encode: fp32 positional-encoding nets encode inside the kernels only"),
            NB_E_UNSUPPORTED;
   DeviceGuard g(m->device);
-  NB_CUDA(launch_encode(m, q, n, x_out, (cudaStream_t)stream));
+  if (m->d.pe_depth > 0)
+    NB_CUDA(launch_encode_pe(m, q, n, x_out, (cudaStream_t)stream));
+  else
+    NB_CUDA(launch_encode(m, q, n, x_out, (cudaStream_t)stream));
   return NB_OK;
 }
 

@@ -15,6 +15,42 @@ bool tc_supported(const nb_desc& d) {
   return enc_k(r) <= d.width;
 }
 
+// nb_encode of a positional-encoding net (R42): the K = 64 layer-1 operand of
+// each record as the kernels build it (encode_cols_pe: fp32 sincospif
+// features, bf16 hi / lo split; hi at [0, d_in), lo at [32, 32 + d_in)),
+// with the three bias ones columns [d_in, d_in + 3) cleared — 64 bf16 per row.
+template <int D0>
+__global__ void k_encode_pe(const float* __restrict__ q, int64_t n, int pe, uint4* __restrict__ out) {
+  const int din = D0 * (1 + pe);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = j < D0 ? q[i * D0 + j] : 0.f;
+    uint32_t c[32];
+    encode_cols_pe<D0>(x, pe, c);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {  // clear the bias ones (elements din .. din + 2)
+      const bool lo_one = 2 * k >= din && 2 * k < din + 3, hi_one = 2 * k + 1 >= din && 2 * k + 1 < din + 3;
+      c[k] &= (lo_one ? 0xFFFF0000u : 0xFFFFFFFFu) & (hi_one ? 0x0000FFFFu : 0xFFFFFFFFu);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) out[8 * i + g] = make_uint4(c[4 * g], c[4 * g + 1], c[4 * g + 2], c[4 * g + 3]);
+  }
+}
+
+cudaError_t launch_encode_pe(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  switch (m->d0) {
+    case 2: k_encode_pe<2><<<blocks, 256, 0, st>>>(q, n, m->d.pe_depth, (uint4*)out); break;
+    case 3: k_encode_pe<3><<<blocks, 256, 0, st>>>(q, n, m->d.pe_depth, (uint4*)out); break;
+    case 4: k_encode_pe<4><<<blocks, 256, 0, st>>>(q, n, m->d.pe_depth, (uint4*)out); break;
+    case 6: k_encode_pe<6><<<blocks, 256, 0, st>>>(q, n, m->d.pe_depth, (uint4*)out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // NB_TRACE builds: device buffer set by nb_debug_set_trace (tools/trace_fwd.py).
 unsigned long long* g_trace_buffer = nullptr;
 static bool g_no_fold = false;

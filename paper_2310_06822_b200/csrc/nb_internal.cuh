@@ -190,6 +190,7 @@ __host__ __device__ constexpr int64_t img_tile_bytes(int features) { return (int
 
 cudaError_t launch_pack_bf16(const nb_model* m, cudaStream_t s);
 cudaError_t launch_encode(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t s);
+cudaError_t launch_encode_pe(const nb_model* m, const float* q, int64_t n, void* out, cudaStream_t s);
 cudaError_t launch_fwd_simt(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);
 cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaStream_t s);

@@ -751,11 +751,10 @@ def test_bf16_sine_pe_forward_and_counts(name, width, layers, pe, n):
 
 def test_sine_pe_unsupported_paths_fail_loudly():
     """Paths not built fail loudly (NB_E_UNSUPPORTED, never a silent
-    fallback): nb_encode with PE (the kernels encode in place), training of
+    fallback): nb_encode of an fp32 PE net (it encodes in place), training of
     sine / PE nets on CTA pairs (w = 256), sine pair nets with exit heads."""
-    cfg, desc, a, q, y, th = _sine_case("c2", 64, 3, 2, "bf16", 1024)
-    m = nb.Model(desc, DEV)
-    m.set_params(torch.from_numpy(th).float())
+    cfg, desc, a, q, y, th = _sine_case("c2", 64, 3, 2, "fp32", 1024)
+    m = nb.Model(nb.Desc("point", 3, 32, 2, (), "fp32", activation="sine", pe_depth=2), DEV)
     with pytest.raises(nb.NBError) as ei:
         m.encode(cuda(q))
     assert "UNSUPPORTED" in str(ei.value)
@@ -1196,3 +1195,26 @@ def test_4d_training_run_conservative():
     m.calibrate(qd, yd)
     c = m.score(qd, yd)
     assert c["fn"] == 0 and c["fp"] < fp0, (c, fp0)
+
+
+@pytest.mark.parametrize("name,pe", [("c1", 8), ("c2", 4), ("c2", 2)])
+def test_encode_pe_operand(name, pe):
+    """nb_encode of a bf16 PE net returns the K = 64 operand the kernels
+    build (R42): equal to the oracle's (fp64 features rounded to fp32, bf16
+    hi / lo split) except where the kernel's fp32 sincospif differs from the
+    correctly rounded value by an ulp — hi bit-exact on >= 99.9 % of the
+    features, hi + lo within 2^-16 relative everywhere, layout zeros exact."""
+    cfg = nbgen.CONFIGS[name]
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 0, 40000)
+    m = nb.Model(nb.Desc(cfg.kind, cfg.space_dim, 128, 3, (), "bf16", activation="sine", pe_depth=pe), DEV)
+    e = m.encode(cuda(q)).cpu().numpy().view(np.uint16)
+    o = oracle.encode_pe(q.numpy(), pe)
+    din = cfg.record_floats * (1 + pe)
+    assert e.shape == (40000, 64)
+    assert not e[:, din:32].any() and not e[:, 32 + din:].any()
+    assert (e[:, :din] == o[:, :din]).mean() >= 0.999
+    tof = lambda u: torch.from_numpy(u.view(np.int16).astype(np.int32) << 16).view(torch.float32).numpy()  # noqa: E731
+    vg = tof(e[:, :din].copy()).astype(np.float64) + tof(e[:, 32:32 + din].copy())
+    vo = tof(o[:, :din].copy()).astype(np.float64) + tof(o[:, 32:32 + din].copy())
+    # a 1-ulp fp32 feature difference can flip lo's bf16 rounding: 2^-16 relative
+    assert np.all(np.abs(vg - vo) <= 2.0 ** -16 * np.maximum(np.abs(vo), 2.0 ** -10))
