@@ -233,6 +233,17 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
                         int64_t n_global, float alpha, float beta, float lr, nb_step_stats* stats,
                         void* stream);
 
+/* a1-a9 over `steps` consecutive training steps in one call: step t uses rows
+ * [t n_local, (t + 1) n_local) of q [steps n_local][d0] and y, the FN weight
+ * alpha_t = alpha0 + (alpha1 - alpha0) t / (steps - 1) (a10's ramp over this
+ * range), and beta, lr as nb_train_step.  Without a communicator the step
+ * sequence is captured into a CUDA graph on a model-owned stream and
+ * launched once (no per-launch gaps; the results equal `steps` nb_train_step
+ * calls); with one, the steps are issued in stream order.  n_local must be a
+ * multiple of 16 when steps > 1 (aligned batch views).  Asynchronous.      */
+nb_status nb_train_steps(nb_model* m, const float* q, const uint8_t* y, int64_t n_local, int64_t n_global,
+                         int32_t steps, float alpha0, float alpha1, float beta, float lr, void* stream);
+
 /* a10: FN weight of step t of T: alpha_t = 1 + 999 t / (T - 1) (R6);
  * beta_t = 1.                                                               */
 double nb_alpha(int64_t t, int64_t T);

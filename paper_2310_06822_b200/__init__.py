@@ -119,6 +119,7 @@ SIGNATURES = {
     "nb_score_host": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_score_async": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
     "nb_train_step": (C.c_int, [_P, _P, _P, _I64, _I64, _F, _F, _F, _P, _P]),
+    "nb_train_steps": (C.c_int, [_P, _P, _P, _I64, _I64, _I32, _F, _F, _F, _F, _P]),
     "nb_alpha": (_D, [_I64, _I64]),
     "nb_model_set_regularization": (C.c_int, [_P, _F, _F]),
     "nb_schedule_init": (C.c_int, [_P, _I32, _I64, _I64]),
@@ -372,6 +373,17 @@ class Model:
 
     def set_regularization(self, l1: float, l2: float) -> None:
         _check(lib().nb_model_set_regularization(self._h, l1, l2), "nb_model_set_regularization")
+
+    def train_steps(self, q, y, steps: int, alpha0: float, alpha1: float, beta: float = 1.0,
+                    lr: float = 1e-3, n_global: int | None = None):
+        """nb_train_steps: `steps` consecutive batches of q.shape[0] // steps
+        rows (one CUDA graph without a communicator); asynchronous."""
+        n = q.shape[0] // steps
+        if n * steps != q.shape[0] or y.shape[0] != q.shape[0]:
+            raise ValueError("q / y must hold steps equal batches")
+        _check(lib().nb_train_steps(self._h, self._q(q), _dev_ptr(y, torch.uint8, self.device, "y"), n,
+                                    n if n_global is None else n_global, steps, alpha0, alpha1, beta, lr,
+                                    _stream(self.device)), "nb_train_steps")
 
     def train_step(self, q, y, alpha: float, beta: float = 1.0, lr: float = 1e-3,
                    n_global: int | None = None, stats: bool = False):

@@ -395,6 +395,13 @@ void nb_model_destroy(nb_model* m) {
     if (m->ev_done[i]) cudaEventDestroy(m->ev_done[i]);
   }
   if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
+  if (m->graph_stream) cudaStreamSynchronize(m->graph_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (m->graph_exec2[i]) cudaGraphExecDestroy((cudaGraphExec_t)m->graph_exec2[i]);
+    if (m->ev_graph[i]) cudaEventDestroy(m->ev_graph[i]);
+    if (m->ev_graph_done[i]) cudaEventDestroy(m->ev_graph_done[i]);
+  }
+  if (m->graph_stream) cudaStreamDestroy(m->graph_stream);
   if (m->ev_pool) {
     for (int i = 0; i < 2 * nb_model::kEvPool; ++i) cudaEventDestroy(m->ev_pool[i]);
     delete[] m->ev_pool;
@@ -737,16 +744,14 @@ nb_status nb_score_host(const nb_model* m_, const float* qh, const uint8_t* yh, 
   return st;
 }
 
-nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
-                        int64_t n_global, float alpha, float beta, float lr, nb_step_stats* stats,
-                        void* stream) {
+// Validation and scratch sizing of a training step of n_local rows.
+static nb_status train_prepare(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
+                               int64_t n_global, float alpha, float beta, float lr, cudaStream_t s) {
   if (!m || n_local < 0 || n_global < n_local || n_global <= 0 ||
       (n_local > 0 && (!q || !y)))
     return set_error("bad argument"), NB_E_ARG;
   if (!(alpha > 0.f) || !(beta >= 0.f) || !(lr > 0.f)) return set_error("bad alpha/beta/lr"), NB_E_ARG;
   if (n_local > 0 && (!aligned16(q) || !aligned16(y))) return misaligned("nb_train_step");
-  DeviceGuard g(m->device);
-  cudaStream_t s = (cudaStream_t)stream;
   const bool tc = m->d.precision == NB_BF16;
   if (tc && !train_tc_supported(m->d)) {
     set_error("bf16 training not built for width %d / sine / positional encoding", m->d.width);
@@ -766,6 +771,13 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
     if (e != cudaSuccess) return set_error("train scratch: %s", cudaGetErrorString(e)), NB_E_OOM;
     m->train_scratch_bytes = need;
   }
+  return NB_OK;
+}
+
+// The launches of one training step on stream s (no synchronisation).
+static nb_status train_enqueue(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
+                               int64_t n_global, float alpha, float beta, float lr, cudaStream_t s) {
+  const bool tc = m->d.precision == NB_BF16;
   NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
   if (tc) {
     g_err.clear();
@@ -784,6 +796,19 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
   }
   if (tc) NB_CUDA(launch_adam_pack(m, lr, s));
   else NB_CUDA(launch_adam(m, lr, s));
+  return NB_OK;
+}
+
+nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
+                        int64_t n_global, float alpha, float beta, float lr, nb_step_stats* stats,
+                        void* stream) {
+  if (!m) return set_error("null model"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  nb_status st = train_prepare(m, q, y, n_local, n_global, alpha, beta, lr, s);
+  if (st != NB_OK) return st;
+  st = train_enqueue(m, q, y, n_local, n_global, alpha, beta, lr, s);
+  if (st != NB_OK) return st;
   if (stats) {
     if (m->comm) {
       if (comm_allreduce_f64_sum(m, m->d_loss, 1, s)) return NB_E_NCCL;
@@ -799,6 +824,70 @@ nb_status nb_train_step(nb_model* m, const float* q, const uint8_t* y, int64_t n
     stats->loss = l;
     return take_flags(m, s, NB_OK);
   }
+  return NB_OK;
+}
+
+nb_status nb_train_steps(nb_model* m, const float* q, const uint8_t* y, int64_t n_local, int64_t n_global,
+                         int32_t steps, float alpha0, float alpha1, float beta, float lr, void* stream) {
+  if (!m || steps < 1 || !(alpha1 > 0.f)) return set_error("bad argument"), NB_E_ARG;
+  // every step's batch view must stay 16-byte aligned (nb.h "Alignment")
+  if (steps > 1 && (n_local % 16 != 0)) return set_error("nb_train_steps: n_local must be a multiple of 16"), NB_E_ARG;
+  DeviceGuard g(m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  nb_status st = train_prepare(m, q, y, n_local, n_global, alpha0, beta, lr, s);
+  if (st != NB_OK) return st;
+  auto alpha_t = [&](int32_t t) {
+    return steps == 1 ? alpha0 : (float)((double)alpha0 + ((double)alpha1 - alpha0) * t / (double)(steps - 1));
+  };
+  const int64_t d0 = m->d0;
+  if (m->comm || steps == 1) {  // plain stream order (collectives stay outside graphs)
+    for (int32_t t = 0; t < steps; ++t) {
+      st = train_enqueue(m, q + (size_t)t * n_local * d0, y + (size_t)t * n_local, n_local, n_global,
+                         alpha_t(t), beta, lr, s);
+      if (st != NB_OK) return st;
+    }
+    return NB_OK;
+  }
+  // capture the step sequence on the model's graph stream, replay it once
+  if (!m->graph_stream) NB_CUDA(cudaStreamCreateWithFlags(&m->graph_stream, cudaStreamNonBlocking));
+  if (!m->ev_graph[0]) {
+    NB_CUDA(cudaEventCreateWithFlags(&m->ev_graph[0], cudaEventDisableTiming));
+    NB_CUDA(cudaEventCreateWithFlags(&m->ev_graph[1], cudaEventDisableTiming));
+    NB_CUDA(cudaEventCreateWithFlags(&m->ev_graph_done[0], cudaEventDisableTiming));
+    NB_CUDA(cudaEventCreateWithFlags(&m->ev_graph_done[1], cudaEventDisableTiming));
+  }
+  // two executable graphs alternate: the one from two calls ago has finished
+  // (its completion event) before it is released, so this call's capture on
+  // the host overlaps the previous call's execution on the device
+  const int slot = m->graph_slot;
+  m->graph_slot ^= 1;
+  if (m->graph_exec2[slot]) {
+    NB_CUDA(cudaEventSynchronize(m->ev_graph_done[slot]));
+    cudaGraphExecDestroy((cudaGraphExec_t)m->graph_exec2[slot]);
+    m->graph_exec2[slot] = nullptr;
+  }
+  cudaStream_t cs = m->graph_stream;
+  NB_CUDA(cudaEventRecord(m->ev_graph[0], s));
+  NB_CUDA(cudaStreamWaitEvent(cs, m->ev_graph[0], 0));
+  NB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int32_t t = 0; t < steps && st == NB_OK; ++t)
+    st = train_enqueue(m, q + (size_t)t * n_local * d0, y + (size_t)t * n_local, n_local, n_global, alpha_t(t),
+                       beta, lr, cs);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  if (st != NB_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ec != cudaSuccess) return cuda_fail(ec, "nb_train_steps: capture");
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return cuda_fail(ei, "nb_train_steps: instantiate");
+  m->graph_exec2[slot] = exec;
+  NB_CUDA(cudaGraphLaunch(exec, cs));
+  NB_CUDA(cudaEventRecord(m->ev_graph_done[slot], cs));
+  NB_CUDA(cudaStreamWaitEvent(s, m->ev_graph_done[slot], 0));
   return NB_OK;
 }
 

@@ -113,6 +113,12 @@ struct nb_model {
   // hierarchy scratch (nb_hier_score, held by the root node; grown on demand)
   void* hier_scratch = nullptr;
   size_t hier_scratch_bytes = 0;
+  // nb_train_steps: the captured step sequence (CUDA graph) and its stream
+  cudaStream_t graph_stream = nullptr;
+  void* graph_exec2[2] = {nullptr, nullptr};  // cudaGraphExec_t of the last two calls
+  int graph_slot = 0;
+  cudaEvent_t ev_graph[2] = {nullptr, nullptr};
+  cudaEvent_t ev_graph_done[2] = {nullptr, nullptr};
   // host-buffer serving path
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};

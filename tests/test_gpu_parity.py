@@ -1218,3 +1218,32 @@ def test_encode_pe_operand(name, pe):
     vo = tof(o[:, :din].copy()).astype(np.float64) + tof(o[:, 32:32 + din].copy())
     # a 1-ulp fp32 feature difference can flip lo's bf16 rounding: 2^-16 relative
     assert np.all(np.abs(vg - vo) <= 2.0 ** -16 * np.maximum(np.abs(vo), 2.0 ** -10))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_train_steps_graph_equals_step_loop(name):
+    """nb_train_steps (the step sequence captured in one CUDA graph) leaves
+    exactly the parameters, Adam state and gradient of the same number of
+    nb_train_step calls with the same batches and alpha ramp; two
+    consecutive calls (re-capture, bias corrections of later steps) too."""
+    cfg = nbgen.CONFIGS[name]
+    T, B = 6, 2048
+    q = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, 2 * T * B)
+    y = labels_oracle(cfg, q.numpy())
+    qd, yd = cuda(q), cuda(y)
+    th = scaled_params(cfg, 17)
+    a = nb.Model(desc_of(cfg), DEV)
+    b = nb.Model(desc_of(cfg), DEV)
+    a.set_params(th)
+    b.set_params(th)
+    for c in range(2):
+        for t in range(T):
+            r = (c * T + t) * B
+            a.train_step(qd[r:r + B], yd[r:r + B], alpha=2.0 + 98.0 * t / (T - 1), beta=0.9, lr=2e-3)
+        b.train_steps(qd[c * T * B:(c + 1) * T * B], yd[c * T * B:(c + 1) * T * B], T, 2.0, 100.0, beta=0.9, lr=2e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(a.get_params(), b.get_params())
+    assert torch.equal(a.get_grad(), b.get_grad())
+    ma, va, sa = a.get_adam()
+    mb, vb, sb = b.get_adam()
+    assert sa == sb == 2 * T and torch.equal(ma, mb) and torch.equal(va, vb)

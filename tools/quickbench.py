@@ -47,7 +47,7 @@ def run(mode):
         m.score_async(q, y, out)
 
 
-for mode in ["forward", "score"]:
+for mode in (os.environ.get("NB_QB_MODES", "forward,score").split(",")):
     for _ in range(3):
         run(mode)
     ks, ss = [], []
