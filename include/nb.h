@@ -303,9 +303,8 @@ nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uin
 void      nb_grid_destroy(nb_grid* g);
 /* y[i] = g(record i) exactly: point lookup, fp64 DDA for rays, SAT for boxes,
  * fp64 voxel-corner cut test for planes (R15-R17, R19; g = any f
- * over the region).  Rays, planes (lines) and boxes: 2D and 3D grids
- * (4D rays / planes / boxes: NB_E_UNSUPPORTED, the tests label them with
- * the oracle).                                                             */
+ * over the region).  Rays, planes (lines) and boxes: 2D, 3D and 4D
+ * grids (4D: the space-time cells of [frames][R][R][R], R48).              */
 nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
                    void* stream);
 

@@ -1021,6 +1021,10 @@ nb_status nb_grid_create(int32_t space_dim, int32_t R, int32_t frames, const uin
     e = launch_sat2_build(gr, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
+  if (e == cudaSuccess && space_dim == 4) {  // 4D boxes / hyperplanes (R48)
+    e = launch_grid4_build(gr, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
   if (e != cudaSuccess) {
     nb_grid_destroy(gr);
     return cuda_fail(e, "nb_grid_create");
@@ -1041,11 +1045,9 @@ void nb_grid_destroy(nb_grid* g) {
 nb_status nb_label(const nb_grid* g, int32_t kind, const float* q, int64_t n, uint8_t* y,
                    void* stream) {
   if (!g || n < 0 || (n > 0 && (!q || !y))) return set_error("bad argument"), NB_E_ARG;
-  if (kind == NB_POINT) {
-    // ok for any dim
-  } else if (g->space_dim == 4 || (kind != NB_RAY && kind != NB_BOX && kind != NB_PLANE)) {
-    set_error("GPU labeller supports points (2D/3D/4D) and 2D/3D rays, planes and boxes");
-    return NB_E_UNSUPPORTED;
+  if (kind != NB_POINT && kind != NB_RAY && kind != NB_BOX && kind != NB_PLANE) {
+    set_error("GPU labeller: unknown query kind");
+    return NB_E_ARG;
   }
   if (n == 0) return NB_OK;
   DeviceGuard dg(g->device);

@@ -222,6 +222,7 @@ cudaError_t launch_label(const nb_grid* g, int kind, const float* q, int64_t n, 
 cudaError_t launch_sat_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_blk_build(nb_grid* g, cudaStream_t s);
 cudaError_t launch_sat2_build(nb_grid* g, cudaStream_t s);
+cudaError_t launch_grid4_build(nb_grid* g, cudaStream_t s);  // 4D SAT + block flags (R48)
 cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* parent, const float* q,
                        const uint8_t* y, int64_t n, unsigned long long* h_counts /*[5]*/, cudaStream_t st,
                        cudaError_t (*forward)(const nb_model*, const float*, int64_t,

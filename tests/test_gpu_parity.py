@@ -1247,3 +1247,26 @@ def test_train_steps_graph_equals_step_loop(name):
     ma, va, sa = a.get_adam()
     mb, vb, sb = b.get_adam()
     assert sa == sb == 2 * T and torch.equal(ma, mb) and torch.equal(va, vb)
+
+
+@pytest.mark.parametrize("kind,n", [("ray", 1 << 16), ("box", 1 << 16), ("plane", 1 << 13)])
+def test_labeller_4d_bit_exact(kind, n):
+    """P6 for 4D rays / hyperplanes / boxes (R48): the GPU labeller (4-axis
+    fp64 DDA, 4D summed-area table, block-pruned 16-corner cut test) equals
+    the oracle on the c4 scene, with axis-aligned rays / hyperplanes through
+    cell faces added."""
+    cfg = nbgen.EXTRA_CONFIGS["c4" + kind]
+    q = nbgen.make_queries(cfg, nbgen.TAG_HOLDOUT, 0, n).numpy()
+    rng = np.random.default_rng(4)
+    extra = np.zeros((512, 8), np.float32)
+    res = np.array([64, 64, 64, 32])
+    extra[:, :4] = np.round(rng.random((512, 4)) * res) / res
+    extra[:, 4:] = np.eye(4)[rng.integers(0, 4, 512)] * rng.choice([-1, 1], (512, 1))
+    if kind == "box":
+        extra[:, 4:] = np.minimum(1.0, extra[:, :4] + rng.random((512, 4)) * 0.1)
+    q = np.concatenate([q, extra], 0)
+    y_ref = labels_oracle(cfg, q)
+    g = nb.Grid(torch.from_numpy(grid_of(cfg)), 4, DEV)
+    y = g.label(kind, cuda(torch.from_numpy(q))).cpu().numpy()
+    assert np.array_equal(y, y_ref), int((y != y_ref).sum())
+    assert 0 < y.mean() < 1
