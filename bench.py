@@ -227,12 +227,26 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": f"{CONFIG}: {WORKLOAD[CONFIG]}; oracle sample of {n} queries per step",
                    "global_batch": n},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
+                         "precision": "fp64",
                          "sample": f"{n} {CONFIG} EVAL queries, fp64 forward + calibrated score"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0, "counts_sample": {k: c[k] for k in ("tp", "fp", "fn", "tn")},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_model() -> str:
+    """The host CPU model (BASELINE.md §3 asks for it beside the core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline_sample(n=1 << 18):
@@ -253,7 +267,8 @@ def cpu_baseline_sample(n=1 << 18):
     tau, _ = oracle.calibrate(z, y)
     oracle.score(z, y, tau)
     t = time.perf_counter() - t0
-    return {"value": n / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    return {"value": n / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "cpu": cpu_model(),
+            "precision": "fp64",
             "sample": f"{n} {CONFIG} EVAL queries: fp64 forward + calibrate + score ({t:.1f} s)"}
 
 
