@@ -55,6 +55,10 @@ KERNEL = {"c2": "k_fwd_tc<64,4,0,0,kScore,d0=3,BF>", "c3": "k_fwd_tc<128,4,0,0,k
           "c4": "k_score_exit<2,{records,image,image},{head1,head2,output}> (early-exit compaction, "
                 "3 segment kernels per 2^24-row chunk)",
           "c5": "k_fwd_tc2p<4,kScore,d0=6> (pipelined CTA pairs)"}
+# launched by torch.distributed.run (WORLD_SIZE set): process group + the
+# model's NCCL communicator at every world size, N = 1 included (the same
+# data-parallel path, a one-rank allreduce per call)
+DIST = "WORLD_SIZE" in os.environ
 METRIC = "bounding queries/s"
 UNIT = "queries/s"
 # bounded oracle samples (about 10 s of host work per step at 16 cores)
@@ -282,13 +286,13 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if DIST:
         dist.init_process_group("nccl", device_id=dev)
     cfg = nbgen.CONFIGS[CONFIG]
     desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
                    cfg.precision)
     m = nb.Model(desc, local)
-    if world > 1:
+    if DIST:
         from paper_2310_06822_b200.dist import comm_init
 
         comm_init(m)
@@ -328,7 +332,7 @@ def run_ours(args):
     m.kernel_time()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    if world > 1:
+    if DIST:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -339,13 +343,13 @@ def run_ours(args):
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     assert all(m.counts_dict(out[i]) == c for i in range(args.steps)), "per-step counts differ"
-    if world > 1:
+    if DIST:
         dist.barrier()
     kernel_ms, launches = m.kernel_time()
     m.set_timing(False)
     dev_ms = sum(a.elapsed_time(b) for a, b in evs)
     t = torch.tensor([dev_ms, kernel_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if DIST:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms, kernel_ms = t.tolist()
     n_total = N_STEP[CONFIG] if strong else n * world
@@ -393,7 +397,7 @@ def run_ours(args):
     y_h = y.cpu().pin_memory()
     for _ in range(2):
         m.score_host(q_h, y_h)
-    if world > 1:
+    if DIST:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -403,7 +407,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if DIST:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = total_q / (e2e_ms.item() * 1e-3)
     assert ce == c, (ce, c)
@@ -445,7 +449,7 @@ def run_ours(args):
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_sample or CPU_SAMPLE[CONFIG])
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if DIST:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -465,7 +469,7 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
     desc = nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
                    cfg.precision)
     m = nb.Model(desc, local)
-    if world > 1:
+    if DIST:
         from paper_2310_06822_b200.dist import comm_init
 
         comm_init(m)
@@ -481,7 +485,7 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
         m.train_step(q_all[t * b:(t + 1) * b], y_all[t * b:(t + 1) * b], alpha=1.0, n_global=B)
 
     def timed(fn):
-        if world > 1:
+        if DIST:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -490,7 +494,7 @@ def train_rate(nb, nbgen, cfg, local, rank, world, steps):
         e1.record()
         torch.cuda.synchronize()
         ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if DIST:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return ms.item()
 
