@@ -3,6 +3,7 @@ calibrated and scored (VERDICT r1 "BJ recipes end to end").
 
     python tools/recipes.py [--configs c1,c2,c3,c4,c5] [--out profiles/r2_recipes.json]
     torchrun --nproc-per-node N tools/recipes.py --configs c5    (data parallel)
+    python tools/recipes.py --configs c4ray,c4box,c4plane    (NEXT-3 4D records, R48)
 
 Per config: Xavier init (nbgen), the recipe's Adam steps of Eq. (1) through
 nb_train_step (c1: 200 x 4096 slices of the 65,536 labelled points, R9; c2,
@@ -71,8 +72,12 @@ def score_in_chunks(m, cfg, grid, tag, n, rank, world, dev, chunk=1 << 26):
     return tot
 
 
-def run(name, rank, world, local, log_every):
-    cfg = nbgen.CONFIGS[name]
+def run(name, rank, world, local, log_every, steps=0):
+    cfg = nbgen.CONFIGS[name] if name in nbgen.CONFIGS else nbgen.EXTRA_CONFIGS[name]
+    if steps:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, train_steps=steps)
     dev = f"cuda:{local}"
     m = nb.Model(nb.Desc(cfg.kind, cfg.space_dim, cfg.width, cfg.hidden_layers, tuple(cfg.head_after),
                          cfg.precision), local)
@@ -144,6 +149,7 @@ def main():
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_recipes.json"))
     ap.add_argument("--log-every", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=0, help="override the recipe's step count (0: the recipe's)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -154,7 +160,7 @@ def main():
     res = {"gpu": torch.cuda.get_device_name(local), "ranks": world, "results": []}
     with ClockSampler(local) as clk:
         for name in args.configs.split(","):
-            r = run(name, rank, world, local, args.log_every)
+            r = run(name, rank, world, local, args.log_every, args.steps)
             res["results"].append(r)
             if rank == 0:
                 print(json.dumps({k: r[k] for k in ("config", "train_device_ms", "calibration_set", "holdout")}),
