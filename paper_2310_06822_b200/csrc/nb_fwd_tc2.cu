@@ -797,6 +797,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
               for (int q4 = 0; q4 < 4; ++q4)
                 *reinterpret_cast<uint4*>(base + ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
                     make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+              if (p.a.tr.c_img[l]) {  // ReLU'(h) bit mask of my 32 features for the backward (R25, R34)
+                uint32_t mw = 0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  mw |= ((pk[j] & 0x7FFFu) ? 1u : 0u) << (2 * j) | ((pk[j] & 0x7FFF0000u) ? 1u : 0u) << (2 * j + 1);
+                reinterpret_cast<uint32_t*>(p.a.tr.c_img[l] + (2 * tile + rank) * 4096)[(f0 / 32) * 128 + rit] = mw;
+              }
             }
           }
           if (last) {

@@ -156,7 +156,8 @@ enum Mode { kForward = 0, kCalibrate = 1, kScore = 2, kTrain = 3 };
 struct TrainArgs {
   uint8_t* x_img;                // encoded layer-1 input, F = 16
   uint8_t* h_img[kMaxLayers];    // h_l (post-activation, bf16), F = w, l = 1..L
-  uint8_t* c_img[kMaxLayers];    // sine nets: cos(z_l) (bf16), F = w — the activation derivative
+  uint8_t* c_img[kMaxLayers];    // sine nets: cos(z_l) (bf16), F = w — the activation derivative;
+                                 // w = 256 ReLU: h_l > 0 bit masks (4 KB per row tile) for k_bwd_tc2p
   uint8_t* hd_img;               // [dL/dz, dL/de_1, dL/de_2, 0..] bf16, F = 8
   float* g32;                    // fp32 [n][3]: dL/dz, dL/de_1, dL/de_2
   float alpha, beta, inv_b;      // Eq. (1) weights, 1 / n_global
@@ -212,7 +213,8 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
                             int64_t n_global, float alpha, float beta, cudaStream_t s);
 bool train_tc_supported(const nb_desc& d);
 cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8_t* const* d_img,
-                           const float* g32, int64_t n, cudaStream_t st);
+                           const float* g32, int64_t n, cudaStream_t st,
+                           const uint8_t* const* m_img = nullptr);  // h_l > 0 bit masks (pipelined)
 size_t train_tc_scratch_bytes(const nb_model* m, int64_t n);
 size_t train_simt_scratch_bytes(const nb_model* m, int64_t n);
 cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s);

@@ -494,7 +494,9 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
   t.x_img = take(T * img_tile_bytes((int)m->pl.k_of[0]));
   for (int l = 0; l < L; ++l) t.h_img[l] = take(T * img_tile_bytes(W));
   const bool sine = m->d.activation == NB_SINE;
-  for (int l = 0; l < L; ++l) t.c_img[l] = sine ? take(T * img_tile_bytes(W)) : 0;
+  // sine nets: cos(z_l) images; w = 256 ReLU (CTA pairs): the backward's bit masks
+  const bool masks = !sine && m->pl.pairs == 2 && m->d.n_heads == 0;
+  for (int l = 0; l < L; ++l) t.c_img[l] = sine ? take(T * img_tile_bytes(W)) : (masks ? take(T * 4096) : 0);
   for (int l = 0; l < L; ++l) t.d_img[l] = take(T * img_tile_bytes(W));
   // the dW GEMM reads 128 features of A per tile: pad the last tile's images
   take(img_tile_bytes(128));
@@ -579,7 +581,7 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
   a.tr.x_img = base + tl.x_img;
   const bool sine = m->d.activation == NB_SINE;
   for (int l = 0; l < L; ++l) a.tr.h_img[l] = base + tl.h_img[l];
-  for (int l = 0; l < L; ++l) a.tr.c_img[l] = sine ? base + tl.c_img[l] : nullptr;
+  for (int l = 0; l < L; ++l) a.tr.c_img[l] = tl.c_img[l] ? base + tl.c_img[l] : nullptr;
   a.tr.hd_img = base + tl.hd_img;
   a.tr.g32 = (float*)(base + tl.g32);
   a.tr.alpha = alpha;
@@ -609,7 +611,11 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
   bp.sine = sine ? 1 : 0;
   bp.g32 = (float*)(base + tl.g32);
   if (pairs)
-    e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st);
+  {
+    const uint8_t* mk[kMaxLayers];
+    for (int l = 0; l < kMaxLayers; ++l) mk[l] = (l < L && tl.c_img[l]) ? base + tl.c_img[l] : nullptr;
+    e = launch_bwd_tc2(m, bp.h_img, bp.d_img, bp.g32, n, st, tl.c_img[0] ? mk : nullptr);
+  }
   else
     e = W == 64 ? launch_bwd<64>(m, bp, st) : launch_bwd<128>(m, bp, st);
   if (e != cudaSuccess) return set_error("backward chain: %s", cudaGetErrorString(e)), e;

@@ -27,6 +27,7 @@ struct BwdParams2 {
   const uint8_t* h_img[kMaxLayers];  // h_1..h_L images (F = 256)
   uint8_t* d_img[kMaxLayers];        // delta_1..delta_L images (F = 256)
   const float* g32;                  // [n][3]
+  const uint32_t* m_img[kMaxLayers]; // pipelined kernel: h_l > 0 bit masks (1024 words per row tile) or NULL
 };
 
 __device__ __forceinline__ uint32_t img_off2(int r, int fg) {
@@ -196,6 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_bwd_tc2(co
 // a_done / b_done; a 17th warp issues the K-steps of D_a over half a's
 // features after a_done, the rest and D_b after b_done.  Arithmetic equals
 // k_bwd_tc2's (R34): same bf16 roundings, fp32 accumulation in the MMA.
+template <bool BITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(const BwdParams2 p) {
   constexpr int W = 256, NEPI = 16, CPT = 32;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -300,11 +302,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(c
         hm[q] = rt < p.num_tiles ? *reinterpret_cast<const uint4*>(hrow + ((f0 / 8 + q) * 16 + rit / 8) * 128 + (rit % 8) * 16)
                                  : make_uint4(0u, 0u, 0u, 0u);
     };
+    // with bit masks (written by the forward) one word per half replaces the h loads
+    constexpr bool bits = BITS;
+    auto load_bits = [&](int64_t rt, int l1, int f0) -> uint32_t {
+      return rt < p.num_tiles ? __ldg(p.m_img[l1 - 1] + rt * 1024 + (f0 / 32) * 128 + rit) : 0u;
+    };
     uint4 hma[4], hmb[4];
+    uint32_t mwa = 0, mwb = 0;
     int64_t t = blockIdx.x / 2;
     if (t < p.num_pairs) {
-      load_mask(hma, 2 * t + rank, L, fa);
-      load_mask(hmb, 2 * t + rank, L, fb);
+      if constexpr (bits) {
+        mwa = load_bits(2 * t + rank, L, fa);
+        mwb = load_bits(2 * t + rank, L, fb);
+      } else {
+        load_mask(hma, 2 * t + rank, L, fa);
+        load_mask(hmb, 2 * t + rank, L, fb);
+      }
     }
     for (; t < p.num_pairs; t += npairs) {
       const int64_t rt = 2 * t + rank;
@@ -329,16 +342,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(c
           }
           const float* gv = reinterpret_cast<const float*>(v);
           uint4 (&hm)[4] = h ? hmb : hma;
+          uint32_t& mw = h ? mwb : mwa;
           uint32_t pk[16];
+          if constexpr (bits) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t hw[4] = {hm[q].x, hm[q].y, hm[q].z, hm[q].w};
+            for (int j = 0; j < 16; ++j)
+              pk[j] = pack_bf16x2(((mw >> (2 * j)) & 1u) ? gv[2 * j] : 0.f, ((mw >> (2 * j + 1)) & 1u) ? gv[2 * j + 1] : 0.f);
+          } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 8 * q + 2 * e;
-              const float m0 = (hw[e] & 0x7FFFu) ? gv[i] : 0.f;  // h > 0 (h >= 0 by ReLU)
-              const float m1 = (hw[e] & 0x7FFF0000u) ? gv[i + 1] : 0.f;
-              pk[4 * q + e] = pack_bf16x2(m0, m1);
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t hw[4] = {hm[q].x, hm[q].y, hm[q].z, hm[q].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = 8 * q + 2 * e;
+                const float m0 = (hw[e] & 0x7FFFu) ? gv[i] : 0.f;  // h > 0 (h >= 0 by ReLU)
+                const float m1 = (hw[e] & 0x7FFF0000u) ? gv[i + 1] : 0.f;
+                pk[4 * q + e] = pack_bf16x2(m0, m1);
+              }
             }
           }
           if (have) {
@@ -350,8 +370,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(c
           }
           if (l >= 2) tmem_st16(trow + acol(s & 1u) + (uint32_t)(f0 / 2), pk);
           // the next stage's mask (layer l - 1 of this tile, or layer L of the next)
-          if (l > 1) load_mask(hm, rt, l - 1, f0);
-          else if (tn < p.num_pairs) load_mask(hm, 2 * tn + rank, L, f0);
+          if constexpr (bits) {
+            if (l > 1) mw = load_bits(rt, l - 1, f0);
+            else if (tn < p.num_pairs) mw = load_bits(2 * tn + rank, L, f0);
+          } else {
+            if (l > 1) load_mask(hm, rt, l - 1, f0);
+            else if (tn < p.num_pairs) load_mask(hm, 2 * tn + rank, L, f0);
+          }
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
@@ -371,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(c
 }
 
 cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8_t* const* d_img,
-                           const float* g32, int64_t n, cudaStream_t st) {
+                           const float* g32, int64_t n, cudaStream_t st, const uint8_t* const* m_img) {
   BwdParams2 p;
   p.packed_bwd = m->packed_bwd;
   p.bl = m->bl;
@@ -387,14 +412,17 @@ cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8
     p.d_img[l] = l < p.L ? d_img[l] : nullptr;
   }
   p.g32 = g32;
+  for (int l = 0; l < kMaxLayers; ++l)
+    p.m_img[l] = (m_img && l < p.L) ? reinterpret_cast<const uint32_t*>(m_img[l]) : nullptr;
   if (p.num_pairs == 0) return cudaSuccess;
   const size_t smem = ((m->bl.bytes + 15) & ~15u) + 64;
   const int pairs = (int)std::min<int64_t>(p.num_pairs, m->num_sms / 2);
   static const bool single = getenv("NB_TC2_SINGLE") != nullptr;  // measurement switch
   if (p.nh == 0 && p.L >= 2 && !single) {  // pipelined halves
-    cudaError_t e = cudaFuncSetAttribute(k_bwd_tc2p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = p.m_img[0] ? k_bwd_tc2p<true> : k_bwd_tc2p<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_bwd_tc2p<<<2 * pairs, 544, smem, st>>>(p);
+    kern<<<2 * pairs, 544, smem, st>>>(p);
     return cudaGetLastError();
   }
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
