@@ -1,7 +1,7 @@
 // nb_adam.cuh — Adam (PyTorch semantics, "Adam ... 1e-3", R8)
 // fused with the bf16 re-pack of one parameter, shared by k_adam_pack
-// (nb_simt.cu) and the fused training kernel's in-kernel finalisation
-// (nb_train_fused.cu).  Product code only (no relation to oracle/).
+// (nb_simt.cu, after a gradient allreduce) and the gradient reduce k_dw_reduce
+// (nb_train_tc.cu, no communicator).  Product code only (no relation to oracle/).
 #pragma once
 #include <cuda_bf16.h>
 
@@ -38,6 +38,10 @@ __device__ __forceinline__ float reg_grad(float t, float l1, float l2) {
 struct AdamArgs {
   float lr_over_bc1, inv_sqrt_bc2, b1, b2, eps, l1, l2;
 };
+
+// Host: advance the model's Adam step counter and fill the step's arguments
+// (bias corrections of step t, the model's pack layout) — nb_simt.cu.
+void adam_setup(nb_model* m, float lr, AdamArgs* h, PackArgs* a);
 
 __device__ __forceinline__ void store_bf16(uint8_t* img, int K, int n, int k, float v) {
   reinterpret_cast<__nv_bfloat16*>(img)[(int64_t)(n / 8) * (K / 8) * 64 + (k / 8) * 64 + (n % 8) * 8 +

@@ -781,7 +781,14 @@ static nb_status train_enqueue(nb_model* m, const float* q, const uint8_t* y, in
   NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
   if (tc) {
     g_err.clear();
-    const cudaError_t e = launch_train_tc(m, q, y, n_local, n_global, alpha, beta, s);
+    // without a communicator the reduced gradient is final: Adam rides in the reduce
+    // Adam inside the gradient reduce saves a launch while the reduce is
+    // latency-bound; above ~2^17 parameters the reduce's element order
+    // (D row fastest) makes the Adam loads strided and the separate
+    // coalesced k_adam_pack wins (measured: c2/c3 -2/-4 us, c5 +9 us)
+    static const bool no_fuse = getenv("NB_ADAM_SEPARATE") != nullptr;  // measurement switch
+    const bool fuse = !m->comm && !no_fuse && m->P <= (1 << 17);
+    const cudaError_t e = launch_train_tc(m, q, y, n_local, n_global, alpha, beta, fuse ? lr : 0.f, s);
     if (e != cudaSuccess) {  // keep the failing stage's detail
       const std::string stage = g_err;
       cuda_fail(e, "nb_train_step");
@@ -794,8 +801,8 @@ static nb_status train_enqueue(nb_model* m, const float* q, const uint8_t* y, in
   if (m->comm) {
     if (comm_allreduce_f32_sum(m, m->grad, m->P, s)) return NB_E_NCCL;
   }
-  if (tc) NB_CUDA(launch_adam_pack(m, lr, s));
-  else NB_CUDA(launch_adam(m, lr, s));
+  if (tc && (m->comm || m->P > (1 << 17) || getenv("NB_ADAM_SEPARATE"))) NB_CUDA(launch_adam_pack(m, lr, s));
+  else if (!tc) NB_CUDA(launch_adam(m, lr, s));
   return NB_OK;
 }
 

@@ -573,6 +573,13 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
             for (int i = 0; i < 4; ++i)
               *reinterpret_cast<uint4*>(base + ((fg0 + i) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
                   make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            if (!(EXT && p.act == NB_SINE) && p.a.tr.c_img[l]) {  // [h > 0] bits for the backward
+              uint32_t mw = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                mw |= ((pk[j] & 0x7FFFu) ? 1u : 0u) << (2 * j) | ((pk[j] & 0x7FFF0000u) ? 1u : 0u) << (2 * j + 1);
+              reinterpret_cast<uint32_t*>(p.a.tr.c_img[l] + tile * (W * 16))[(col0 + 32 * c) / 32 * 128 + rit] = mw;
+            }
             if (EXT && p.act == NB_SINE) {  // sigma'(z) = cos z for the backward chain (R41)
               uint32_t ck[16];
 #pragma unroll

@@ -157,7 +157,8 @@ struct TrainArgs {
   uint8_t* x_img;                // encoded layer-1 input, F = 16
   uint8_t* h_img[kMaxLayers];    // h_l (post-activation, bf16), F = w, l = 1..L
   uint8_t* c_img[kMaxLayers];    // sine nets: cos(z_l) (bf16), F = w — the activation derivative;
-                                 // w = 256 ReLU: h_l > 0 bit masks (4 KB per row tile) for k_bwd_tc2p
+                                 // ReLU: h_l > 0 bit masks (W * 16 B per row tile, word (f / 32) * 128 + row)
+                                 // for the backward (k_bwd_tc / k_bwd_tc2p), NULL for CTA pairs with heads
   uint8_t* hd_img;               // [dL/dz, dL/de_1, dL/de_2, 0..] bf16, F = 8
   float* g32;                    // fp32 [n][3]: dL/dz, dL/de_1, dL/de_2
   float alpha, beta, inv_b;      // Eq. (1) weights, 1 / n_global
@@ -209,8 +210,10 @@ bool simt_supported(const nb_desc& d);
 
 cudaError_t launch_train_simt(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                               int64_t n_global, float alpha, float beta, cudaStream_t s);
+// fuse_lr > 0: the gradient reduce also takes the Adam step + re-pack (no
+// communicator); 0: the caller launches Adam after the allreduce
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
-                            int64_t n_global, float alpha, float beta, cudaStream_t s);
+                            int64_t n_global, float alpha, float beta, float fuse_lr, cudaStream_t s);
 bool train_tc_supported(const nb_desc& d);
 cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8_t* const* d_img,
                            const float* g32, int64_t n, cudaStream_t st,

@@ -651,22 +651,27 @@ __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float
     adam_pack_one(i, g[i], th, m, v, h, a);
 }
 
-cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
+void adam_setup(nb_model* m, float lr, AdamArgs* h, PackArgs* a) {
   m->step += 1;
   const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
   const double bc1 = 1.0 - pow(b1, (double)m->step), bc2 = 1.0 - pow(b2, (double)m->step);
+  a->theta = m->theta;
+  a->out = m->packed;
+  a->out_bwd = m->packed_bwd;
+  a->bl = m->bl;
+  a->pl = m->pl;
+  a->po = m->po;
+  a->W = m->d.width;
+  a->L = m->d.hidden_layers;
+  a->d0 = m->din;
+  a->nh = m->d.n_heads;
+  *h = AdamArgs{(float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1, (float)b2, (float)eps, m->l1, m->l2};
+}
+
+cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
+  AdamArgs h;
   PackArgs a;
-  a.theta = m->theta;
-  a.out = m->packed;
-  a.out_bwd = m->packed_bwd;
-  a.bl = m->bl;
-  a.pl = m->pl;
-  a.po = m->po;
-  a.W = m->d.width;
-  a.L = m->d.hidden_layers;
-  a.d0 = m->din;
-  a.nh = m->d.n_heads;
-  AdamArgs h{(float)(lr / bc1), (float)(1.0 / sqrt(bc2)), (float)b1, (float)b2, (float)eps, m->l1, m->l2};
+  adam_setup(m, lr, &h, &a);
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
   k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P, h, a);
   return cudaGetLastError();

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nb_fwd_tc.cuh"
@@ -44,6 +45,7 @@ struct FusedParams {
   unsigned long long* stats;
   unsigned int* flags;
   float* partial;  // [job][cta][kDwColsF][128]
+  unsigned long long* trace;  // NB_TRACE builds (tools/trace_fused.py)
 };
 constexpr int kFusedW = 64;
 constexpr int kDwColsF = 272;  // = nb_train_tc.cu kDwCols
@@ -361,6 +363,485 @@ __global__ void __launch_bounds__(256, 1) k_train_fused(const FusedParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_train_fused2: the same step with TWO row tiles in flight per CTA.
+// Warps 0-3 run slot 0's epilogues, warps 4-7 slot 1's (warp w owns TMEM lane
+// quarter w % 4 and all 64 columns), warp 8 is the MMA issuer: one thread
+// walks a fixed program — step k of slot 0, step k of slot 1, step k + 1 of
+// slot 0, ... — waiting on each slot's `ready` barrier, so one slot's
+// epilogue overlaps the other's MMAs and the dW accumulation order is fixed
+// (deterministic sums).  The dW GEMMs run transposed, D^T_l += [h_{l-1} | 1]^T
+// delta_l (M = input features + the ones feature, N = 64), so the four
+// accumulators plus the head's ([h_L | 1]^T dz, N = 16) take 272 TMEM columns
+// and both slots' working sets fit beside them:
+//   D_0 [0, 64)  D_1 [64, 128)  A_0 [128, 160)  A_1 [160, 192)  ones [192, 200)
+//   dW job l at 224 + 64 l (l < 4), head at 480 (N = 16).
+// Each slot's shared memory: x image (16 features + ones group), h_0..h_3
+// images (64 features + ones group; h_{L-1} is also the delta image once the
+// head MMA has read it), dz image (16 features, dz in feature 0); the
+// backward takes ReLU' from the h images (read before h_{L-1}'s reuse).  An A
+// operand spans 128 features = 32 KB from its image start: features beyond
+// the image read the next buffer and land in TMEM lanes nobody reads.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kF2X = 24u * 256u;         // x image: 16 features + ones group
+constexpr uint32_t kF2H = 72u * 256u;         // h image: 64 features + ones group
+constexpr uint32_t kF2DZ = 16u * 256u;        // dz image (head B operand, N = 16)
+constexpr uint32_t kF2Slot = kF2X + 4u * kF2H + kF2DZ;
+constexpr uint32_t kF2Pad = 32768u - (kF2H + kF2DZ);  // the last A span (h_3 of slot 1) stays in bounds
+__host__ __device__ constexpr uint32_t f2_off_slot(uint32_t pl_bytes, int s) {
+  return ((pl_bytes + 1023u) & ~1023u) + (uint32_t)s * kF2Slot;
+}
+__host__ __device__ constexpr uint32_t f2_bars(uint32_t pl_bytes) { return f2_off_slot(pl_bytes, 2) + kF2Pad; }
+
+#ifdef NB_TRACE
+extern unsigned long long* g_trace_buffer;
+// tools/trace_fused.py: per CTA 64 (globaltimer, code) events; thread 0 uses
+// [0, 16), slot s's warp 4 s lane 0 uses [16 + 24 s, 40 + 24 s)
+#define NB_TRF(idx, code)                                                           \
+  do {                                                                              \
+    if (p.trace && (idx) < 64) {                                                    \
+      uint64_t t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+      p.trace[((int64_t)blockIdx.x * 64 + (idx)) * 2] = t_;                         \
+      p.trace[((int64_t)blockIdx.x * 64 + (idx)) * 2 + 1] = (unsigned long long)(code); \
+    }                                                                               \
+  } while (0)
+// fine events of CTA 0 (clock64): region r (0 issuer, 1 + s slot s lead lane), 512 each
+#define NB_TRC(region, code)                                                        \
+  do {                                                                              \
+    if (p.trace && blockIdx.x == 0 && trc < 512) {                                  \
+      const int64_t b_ = 148 * 64 * 2 + ((int64_t)(region) * 512 + trc) * 2;        \
+      p.trace[b_] = clock64();                                                      \
+      p.trace[b_ + 1] = (unsigned long long)(code);                                 \
+      ++trc;                                                                        \
+    }                                                                               \
+  } while (0)
+#else
+#define NB_TRF(idx, code) \
+  do {                    \
+  } while (0)
+#define NB_TRC(region, code) \
+  do {                       \
+  } while (0)
+#endif
+
+template <int L>
+__global__ void __launch_bounds__(288, 1) k_train_fused2(const FusedParams p) {
+  constexpr int W = kFusedW;
+  static_assert(L >= 2 && L <= 4, "fused2 plan");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + f2_bars(p.pl.bytes));
+  // [0] weights, [1 + s] ready (TMEM operands), [3 + s] acc, [5 + s] head,
+  // [7 + s] dw, [9 + s] ready (images).  Two ready barriers: consecutive
+  // arrives on one of them are always separated by a wait on an MMA the
+  // issuer launched for the earlier one, so no phase is overrun.
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t w_bar = smem_u32(bars);
+  if (threadIdx.x == 0) NB_TRF(0, 0);
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_init(w_bar, 1);
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(smem_u32(bars + 1 + s), 4);
+        mbar_init(smem_u32(bars + 3 + s), 1);
+        mbar_init(smem_u32(bars + 5 + s), 1);
+        mbar_init(smem_u32(bars + 7 + s), 1);
+        mbar_init(smem_u32(bars + 9 + s), 4);
+      }
+      fence_barrier_init();
+      mbar_arrive_expect_tx(w_bar, p.pl.bytes);
+      for (uint32_t off = 0; off < p.pl.bytes; off += 32768u)
+        bulk_g2s(sbase + off, p.packed + off, min(32768u, p.pl.bytes - off), w_bar);
+    }
+    __syncwarp();
+    tmem_alloc<512>(smem_u32(tmem_slot));
+  }
+  // constant image parts: the ones groups (feature 0 of the group = 1.0), the
+  // dz images (only feature 0 is rewritten per tile) and the pad
+  for (int i = threadIdx.x; i < 2 * 128; i += blockDim.x) {
+    const int s = i >> 7, r = i & 127;
+    const uint32_t so = f2_off_slot(p.pl.bytes, s);
+    const uint4 one = make_uint4(0x3F80u, 0u, 0u, 0u), zero = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(smem + so + fimg(r, 2)) = one;
+    for (int l = 0; l < 4; ++l) *reinterpret_cast<uint4*>(smem + so + kF2X + l * kF2H + fimg(r, 8)) = one;
+    for (int g = 0; g < 2; ++g) *reinterpret_cast<uint4*>(smem + so + kF2X + 4 * kF2H + fimg(r, g)) = zero;
+  }
+  for (uint32_t i = threadIdx.x; i < kF2Pad / 16u; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem + f2_off_slot(p.pl.bytes, 2))[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  NB_CHECK((tmem & 0xFFFFu) == 0u);
+  constexpr uint32_t ONES = 192u, DW0 = 224u, HEAD = 480u;
+  if (warp < 4) {  // forward bias-folding ones block (k = 0, 1, 2 of every row)
+    const uint32_t ones[8] = {0x3F803F80u, 0x00003F80u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tmem_st8(tmem + ((uint32_t)(warp * 32) << 16) + ONES, ones);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  mbar_wait(w_bar, 0);
+  if (threadIdx.x == 0) NB_TRF(1, 1);
+  const int64_t G = gridDim.x;
+  const bool any = (int64_t)blockIdx.x < p.num_tiles;
+  int tri = 16 + 24 * (warp >> 2);  // trace slot of this slot's lead lane
+
+  // Per tile and slot, the epilogue signals `ready` ACTIONS = 3L times; action a
+  // lets the issuer launch:
+  //   0            layer 0 (A = encoded x)              -> acc
+  //   1 .. L-1     layer l (A = h_{l-1} in TMEM)        -> acc
+  //   L            g_{L-2} = delta_{L-1} W_{L-1}        -> acc
+  //   L+1          head: [h_{L-1} | 1]^T dz             -> head
+  //   then per l = L-2 .. 0: dW job l + 1 (delta_{l+1} image written, -> dw)
+  //                and for l >= 1 g_{l-1} = delta_l W_l (-> acc);
+  //   last         dW job 0                              -> dw
+  // The chain (acc) never waits for an image write: TMEM operands are
+  // signalled first; a delta image is written one chain step later, once the
+  // MMA that read the buffer before (head, previous dW job) has finished.
+  constexpr int ACTIONS = 3 * L;
+  if (warp == 8) {
+    // ---------------- MMA issuer (the warp waits, one elected lane issues) ----------------
+    const uint32_t idesc_f = make_idesc_bf16(128, W);          // A TMEM, B K-major
+    const uint32_t idesc_b = make_idesc_bf16(128, W, 0, 1);    // B = W_l read MN-major
+    const uint32_t idesc_dw = make_idesc_bf16(128, 64, 1, 1);  // A, B MN-major images
+    const uint32_t idesc_hd = make_idesc_bf16(128, 16, 1, 1);
+    auto mn_desc = [&](uint32_t off) { return make_sdesc(sbase + off, 128u, 2048u); };
+    uint32_t rph[2] = {0u, 0u}, sph[2] = {0u, 0u};
+    int trc = 0;
+    (void)trc;
+    for (int64_t k = 0;; ++k) {
+      const bool act[2] = {(int64_t)blockIdx.x + 2 * k * G < p.num_tiles,
+                           (int64_t)blockIdx.x + (2 * k + 1) * G < p.num_tiles};
+      if (!act[0]) break;
+#pragma unroll
+      for (int a = 0; a < ACTIONS; ++a) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (!act[s]) continue;
+          const uint32_t so = f2_off_slot(p.pl.bytes, s);
+          const uint32_t D = 64u * s, A = 128u + 32u * s;
+          const uint32_t acc_bar = smem_u32(bars + 3 + s), dw_bar = smem_u32(bars + 7 + s);
+          const bool first = k == 0 && s == 0;  // the CTA's first dW contribution
+          // image actions: head, dW jobs; the rest wait on TMEM operands
+          const bool img = a == L + 1 || a == ACTIONS - 1 || (a >= L + 2 && ((a - (L + 2)) & 1) == 0);
+          if (img) {
+            mbar_wait(smem_u32(bars + 9 + s), sph[s]);
+            sph[s] ^= 1u;
+          } else {
+            mbar_wait(smem_u32(bars + 1 + s), rph[s]);
+            rph[s] ^= 1u;
+          }
+          tc_fence_after();
+          if (lane == 0) NB_TRC(0, 100 * s + a);
+          auto g_mma = [&](int l) {  // g_{l-1} = delta_l W_l (B MN-major: K = out of layer l)
+            const uint64_t bdesc = make_sdesc(sbase + p.pl.off_w[l], (W / 8u) * 128u, 128u);
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk)
+              mma_ts(tmem + D, tmem + A + kk * 8u, bdesc + (uint64_t)((kk * 32u * W) >> 4), idesc_b, kk > 0u);
+            mma_commit(acc_bar);
+          };
+          auto dw_mma = [&](int l) {  // [h_{l-1} | 1]^T delta_l (x image for l = 0); delta image = h_{L-1}'s buffer
+            const uint64_t ad = mn_desc(so + (l == 0 ? 0u : kF2X + (l - 1) * kF2H));
+            const uint64_t bd = mn_desc(so + kF2X + (L - 1) * kF2H);
+#pragma unroll
+            for (uint32_t kk = 0; kk < 8; ++kk)
+              mma_ss(tmem + DW0 + 64u * l, ad + kk * 16u, bd + kk * 16u, idesc_dw, (!first || kk > 0u) ? 1u : 0u);
+            mma_commit(dw_bar);
+          };
+          if (elect_one()) {
+            if (a == 0) {
+              mma_ts(tmem + D, tmem + A, make_sdesc(sbase + p.pl.off_w[0], 128u, (kEncK / 8u) * 128u), idesc_f, 0u);
+              mma_commit(acc_bar);
+            } else if (a < L) {
+              mma_ts(tmem + D, tmem + ONES, make_sdesc(sbase + p.pl.off_bb[a], 128u, (kEncK / 8u) * 128u),
+                     idesc_f, 0u);
+              const uint64_t bd = make_sdesc(sbase + p.pl.off_w[a], 128u, (W / 8u) * 128u);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk) mma_ts(tmem + D, tmem + A + kk * 8u, bd + kk * 16u, idesc_f, 1u);
+              mma_commit(acc_bar);
+            } else if (a == L) {
+              g_mma(L - 1);
+            } else if (a == L + 1) {
+              const uint64_t ad = mn_desc(so + kF2X + (L - 1) * kF2H), bd = mn_desc(so + kF2X + 4 * kF2H);
+#pragma unroll
+              for (uint32_t kk = 0; kk < 8; ++kk)
+                mma_ss(tmem + HEAD, ad + kk * 16u, bd + kk * 16u, idesc_hd, (!first || kk > 0u) ? 1u : 0u);
+              mma_commit(smem_u32(bars + 5 + s));
+            } else if (a < ACTIONS - 1) {
+              const int j = a - (L + 2);  // dW job L-1-j/2 (even j), g_mma(L-2-(j-1)/2) (odd j)
+              if ((j & 1) == 0) dw_mma(L - 1 - j / 2);
+              else g_mma(L - 2 - (j - 1) / 2);
+            } else {
+              dw_mma(0);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps of slot s ----------------
+    const int s = warp >> 2, qw = warp & 3, rit = qw * 32 + lane;
+    const uint32_t so = f2_off_slot(p.pl.bytes, s);
+    const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
+    const uint32_t D = 64u * s, A = 128u + 32u * s;
+    const uint32_t ready = smem_u32(bars + 1 + s), ready_img = smem_u32(bars + 9 + s);
+    const uint32_t acc_bar = smem_u32(bars + 3 + s);
+    const uint32_t head_bar = smem_u32(bars + 5 + s), dw_bar = smem_u32(bars + 7 + s);
+    const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout);
+    const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
+    uint8_t* ximg = smem + so;
+    uint8_t* dimg = smem + so + kF2X + (L - 1) * kF2H;
+    uint8_t* dzimg = smem + so + kF2X + 4 * kF2H;
+    uint32_t aph = 0, hph = 0, dph = 0;
+    int trc = 0;
+    (void)trc;
+    const bool lead = qw == 0 && lane == 0;
+    uint32_t lcnt[4] = {0u, 0u, 0u, 0u};
+    double lsum = 0.0;
+    const int d0 = p.d0;
+    // TMEM operand ready (tcgen05.st done): no shared-memory publication needed
+    auto arrive_tm = [&]() {
+      if (lead) NB_TRC(1 + s, 3);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ready);
+    };
+    // images written: publish the generic-proxy stores to the MMA (async proxy)
+    auto arrive_sm = [&]() {
+      if (lead) NB_TRC(1 + s, 5);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ready_img);
+    };
+    auto wait_acc = [&]() {
+      if (lead) NB_TRC(1 + s, 1);
+      mbar_wait(acc_bar, aph);
+      aph ^= 1u;
+      tc_fence_after();
+      if (lead) NB_TRC(1 + s, 2);
+    };
+    auto wait_dw = [&]() {  // the last dW job issued has read its images
+      mbar_wait(dw_bar, dph);
+      dph ^= 1u;
+    };
+    auto ld64 = [&](uint32_t (&v)[64]) {
+      tmem_ld32(trow + D, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(trow + D + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_wait_ld();
+    };
+    auto put_img = [&](uint8_t* img, const uint32_t (&pk)[32]) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        *reinterpret_cast<uint4*>(img + fimg(rit, g)) = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+    };
+    auto put_a = [&](const uint32_t (&pk)[32]) {
+      tmem_st16(trow + A, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+      tmem_st16(trow + A + 16u, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
+      tmem_wait_st();
+    };
+    // ReLU' (R25): a bf16 half h >= 0 is nonzero iff (h & 0x7FFF) + 0x7FFF
+    // carries into bit 15; the pair mask selects the packed gradient (a masked
+    // half is +0, the same bits as rounding a masked 0)
+    auto pair_mask = [](uint32_t hw) {
+      const uint32_t t = ((hw & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;
+      return (t >> 15) * 0xFFFFu;
+    };
+    // the next tile's record and label are loaded one tile ahead
+    float xn[8];
+    int yn = 0;
+    auto load_x = [&](int64_t t) {
+      const int64_t r = t * kTile + rit;
+      const bool ok = t < p.num_tiles && r < p.n;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xn[j] = (ok && j < d0) ? __ldg(p.q + r * d0 + j) : 0.f;
+      yn = ok ? (int)__ldg(p.y + r) : 0;
+    };
+    int64_t tile = blockIdx.x + (int64_t)s * G;
+    load_x(tile);
+    bool first_tile = true;
+    for (; tile < p.num_tiles; tile += 2 * G) {
+      const bool valid = tile * kTile + rit < p.n;
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = xn[j];
+      const int yv = yn;
+      if (lead) NB_TRF(tri++, 10 + s);
+      load_x(tile + 2 * G);
+      if (!first_tile) wait_dw();  // the previous tile's dW job 0: x, h and delta images free
+      {
+        uint32_t c[8];
+        encode_cols<0, true>(x, d0, c);
+        tmem_st8(trow + A, c);
+#pragma unroll
+        for (int fg = 0; fg < 2; ++fg)
+          *reinterpret_cast<uint4*>(ximg + fimg(rit, fg)) = make_uint4(c[4 * fg], c[4 * fg + 1], c[4 * fg + 2], c[4 * fg + 3]);
+        tmem_wait_st();
+      }
+      arrive_tm();  // action 0 (the x image is published by the head action's arrive)
+      // ---------------- forward ----------------
+      float z = 0.f;
+      uint32_t hL[32];  // h_{L-1}, packed
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        wait_acc();
+        uint32_t v[64];
+        ld64(v);
+        if (lead) NB_TRC(1 + s, 4);
+        if (l == L - 1) {
+          // output head in fp32 (R33), summed as k_train_fused's two column halves
+          float zh[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float za = 0.f, zb = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              za = fmaf(fmaxf(__uint_as_float(v[32 * h + j]), 0.f), wout[32 * h + j], za);
+              zb = fmaf(fmaxf(__uint_as_float(v[32 * h + j + 1]), 0.f), wout[32 * h + j + 1], zb);
+            }
+            zh[h] = za + zb;
+          }
+          z = bout + (zh[0] + zh[1]);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hL[j] = pack_relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        } else {
+          uint32_t pk[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) pk[j] = pack_relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          put_a(pk);
+          arrive_tm();                               // action l + 1
+          put_img(smem + so + kF2X + l * kF2H, pk);  // h_l image (dW, ReLU'), published by a later arrive
+        }
+      }
+      // ---------------- loss gradient and delta_{L-1} ----------------
+      const float yf = (float)yv;
+      const float wgt = valid ? (yv ? p.alpha : p.beta) : 0.f;
+      const float dz = wgt * (__frcp_rn(1.f + __expf(-z)) - yf) * p.inv_b;  // rcp_rn(x) == 1.f / x
+      // pd: the delta whose image (dW operand) is written one chain step later
+      uint32_t pd[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) pd[j] = pack_bf16x2(dz * wout[2 * j], dz * wout[2 * j + 1]) & pair_mask(hL[j]);
+      put_a(pd);
+      arrive_tm();  // action L: g_{L-2}
+      put_img(dimg, hL);  // h_{L-1} image (the head MMA's A)
+      *reinterpret_cast<uint4*>(dzimg + fimg(rit, 0)) = make_uint4(pack_bf16x2(dz, 0.f), 0u, 0u, 0u);
+      arrive_sm();  // action L + 1: head
+      if (lead) NB_TRF(tri++, 20 + s);
+      // ---------------- backward + dW ----------------
+#pragma unroll
+      for (int l = L - 2; l >= 0; --l) {
+        uint4 hv[8];  // h_l image row (ReLU' of layer l)
+#pragma unroll
+        for (int g = 0; g < 8; ++g) hv[g] = *reinterpret_cast<const uint4*>(smem + so + kF2X + l * kF2H + fimg(rit, g));
+        wait_acc();  // g_l = delta_{l+1} W_{l+1}
+        uint32_t v[64];
+        ld64(v);
+        if (lead) NB_TRC(1 + s, 4);
+        // delta_{l+1}'s image once its buffer is free (the head MMA read h_{L-1},
+        // dW job l + 2 read delta_{l+2})
+        if (l == L - 2) {
+          mbar_wait(head_bar, hph);
+          hph ^= 1u;
+        } else {
+          wait_dw();
+        }
+        put_img(dimg, pd);
+        arrive_sm();  // dW job l + 1
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint4 q4 = hv[j >> 2];
+          const uint32_t hw = (j & 3) == 0 ? q4.x : ((j & 3) == 1 ? q4.y : ((j & 3) == 2 ? q4.z : q4.w));
+          pd[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])) & pair_mask(hw);
+        }
+        if (l >= 1) {
+          put_a(pd);
+          arrive_tm();  // g_{l-1}
+        }
+      }
+      wait_dw();  // dW job 1 has read delta_1
+      put_img(dimg, pd);
+      arrive_sm();  // dW job 0
+      {  // loss value and batch counts at z >= 0 (off the chain)
+        const float sp = fmaxf(yv ? -z : z, 0.f) + log1pf(__expf(-fabsf(z)));
+        lsum += (double)(wgt * sp);
+        const bool pred = z >= 0.f, yy = yv != 0;
+        lcnt[0] += __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && yy));
+        lcnt[1] += __popc(__ballot_sync(0xFFFFFFFFu, valid && pred && !yy));
+        lcnt[2] += __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && yy));
+        lcnt[3] += __popc(__ballot_sync(0xFFFFFFFFu, valid && !pred && !yy));
+        if (valid && yv > 1) atomicOr(p.flags, kFlagLabel);
+      }
+      first_tile = false;
+      if (lead) NB_TRF(tri++, 30 + s);
+    }
+    if (!first_tile) {  // the last tile's dW job 0
+      wait_dw();
+      tc_fence_after();
+    }
+    if (lane == 0) {
+      for (int i = 0; i < 4; ++i)
+        if (lcnt[i]) atomicAdd(p.stats + i, (unsigned long long)lcnt[i]);
+    }
+    double ls = lsum;
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
+    if (lane == 0 && ls != 0.0) atomicAdd(p.loss, ls * (double)p.inv_b);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) NB_TRF(2, 2);
+  // dW accumulators -> partials in k_dw_tc's layout ([col][128 D rows] per job
+  // and CTA): TMEM lane f = input feature = partial column, column m = output
+  // row; job 0's meaningful lanes are f <= 16, the others' f <= 64 (ones).
+  if (warp < 8) {
+    const int qw = warp & 3, f = qw * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
+    for (int job = warp >> 2; job <= L; job += 2) {
+      const int fmax = job == 0 ? 16 : 64;
+      if (qw * 32 > fmax) continue;
+      float* out = p.partial + ((int64_t)(job * gridDim.x + blockIdx.x) * kDwColsF + f) * 128;
+      if (job == L) {  // head: column 0 -> D row 0
+        uint32_t w[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+              "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]),
+              "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+            : "r"(trow + HEAD));
+        tmem_wait_ld();
+        if (f <= fmax) out[0] = any ? __uint_as_float(w[0]) : 0.f;
+        continue;
+      }
+      uint32_t v[64];
+      tmem_ld32(trow + DW0 + 64u * job, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(trow + DW0 + 64u * job + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_wait_ld();
+      if (f <= fmax) {
+#pragma unroll
+        for (int m = 0; m < 64; m += 4)
+          *reinterpret_cast<float4*>(out + m) =
+              any ? make_float4(__uint_as_float(v[m]), __uint_as_float(v[m + 1]), __uint_as_float(v[m + 2]),
+                                __uint_as_float(v[m + 3]))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) NB_TRF(3, 3);
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 bool train_fused_supported(const nb_model* m) {
   const nb_desc& d = m->d;
   return d.precision == NB_BF16 && d.width == kFusedW && d.n_heads == 0 && d.hidden_layers >= 2 &&
@@ -373,9 +854,17 @@ size_t train_fused_smem(const nb_model* m) {
   return off_x + 32 * 256 + 4 * 80 * 256 + 128 * 256 + 64 + 128 * 4;
 }
 
+static size_t train_fused2_smem(const nb_model* m) { return f2_bars(m->pl.bytes) + 128; }
+
+// Measurement switch: the one-tile-per-CTA kernel (NB_FUSED1=1).
+static bool fused1_forced() {
+  static const bool v = getenv("NB_FUSED1") != nullptr;
+  return v;
+}
+
 cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                                int64_t n_global, float alpha, float beta, float* partial,
-                               int* cpj, cudaStream_t st) {
+                               int* cpj, int* head_row, cudaStream_t st) {
   FusedParams p;
   memset(&p, 0, sizeof(p));
   p.packed = m->packed;
@@ -393,8 +882,22 @@ cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, in
   p.stats = m->d_stats;
   p.flags = m->d_flags;
   p.partial = partial;
+#ifdef NB_TRACE
+  p.trace = g_trace_buffer;
+#endif
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(p.num_tiles, m->num_sms));
   *cpj = grid;
+  const size_t smem2 = train_fused2_smem(m);
+  if (!fused1_forced() && smem2 <= 227 * 1024) {
+    // two tiles in flight; the dW accumulators are transposed (head gradient in D row 0)
+    *head_row = 0;
+    auto kern = p.L == 4 ? k_train_fused2<4> : (p.L == 3 ? k_train_fused2<3> : k_train_fused2<2>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 288, smem2, st>>>(p);
+    return cudaGetLastError();
+  }
+  *head_row = 64;  // the head gradient rides in row 64 of the last layer's delta image
   const size_t smem = train_fused_smem(m);
   auto kern = p.L == 4 ? k_train_fused<4> : k_train_fused<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -19,6 +19,7 @@
 
 #include <cstdlib>
 
+#include "nb_adam.cuh"
 #include "nb_device.cuh"
 #include "nb_internal.cuh"
 
@@ -38,6 +39,7 @@ struct BwdParams {
   uint8_t* d_img[kMaxLayers];        // delta_1..delta_L images (F = W)
   const float* g32;                  // [n][3]
   const uint8_t* c_img[kMaxLayers];  // sine nets: cos(z_l) images; delta = g * cos (R41)
+  const uint32_t* m_img[kMaxLayers]; // ReLU nets: h_l > 0 bit masks (W * 4 words per row tile) or NULL
   int sine;
 };
 
@@ -47,7 +49,7 @@ __device__ __forceinline__ uint32_t img_off(int r, int fg) {
 
 // NSLOT tiles in flight, 4 warps (one per TMEM lane quarter) per slot, each
 // thread owns one row and walks its W columns in 32-column chunks.
-template <int W>
+template <int W, bool BITS>
 __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   constexpr int NSLOT = 2, WPS = 4;
   constexpr int COLS = (NSLOT * (W + W / 2) <= 256) ? 256 : 512;
@@ -95,11 +97,19 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
   // Global-memory latency is kept off the per-layer chain: each thread's h row
   // of the next layer (ReLU masks) and the next tile's dL/dz are loaded one
   // step ahead into registers.
-  constexpr int HW = W / 8;  // uint4 per h row
+  // BITS: the forward's bit masks (word c of a row = [h_l > 0] of features
+  // 32c .. 32c + 31) replace the h rows: 16 B instead of 2W B per row and layer.
+  constexpr int HW = BITS ? 1 : W / 8;  // uint4 per h row
+  constexpr int MW = W / 32;            // mask words per row
   auto load_h = [&](uint4 (&h)[HW], int l1, int64_t t) {  // h_{l1} row of tile t (l1 1-based)
     const uint8_t* hrow = (p.sine ? p.c_img[l1 - 1] : p.h_img[l1 - 1]) + t * img_tile_bytes(W);
 #pragma unroll
     for (int q = 0; q < HW; ++q) h[q] = *reinterpret_cast<const uint4*>(hrow + img_off(rit, q));
+  };
+  auto load_m = [&](uint32_t (&mk)[MW], int l1, int64_t t) {
+    const uint32_t* mrow = p.m_img[l1 - 1] + t * (W * 4) + rit;
+#pragma unroll
+    for (int c = 0; c < MW; ++c) mk[c] = __ldg(mrow + c * 128);
   };
   auto load_g = [&](float (&gg)[3], int64_t t) {
     const int64_t r = t * kTile + rit;
@@ -108,10 +118,12 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
     for (int k = 0; k < 3; ++k) gg[k] = valid ? p.g32[r * 3 + k] : 0.f;
   };
   uint4 hcur[HW], hnext[HW];
+  uint32_t mcur[MW], mnext[MW];
   float gcur[3], gnext[3];
   int64_t tile = blockIdx.x + (int64_t)s * G;
   if (tile < p.num_tiles) {
-    load_h(hcur, p.L, tile);
+    if (BITS) load_m(mcur, p.L, tile);
+    else load_h(hcur, p.L, tile);
     load_g(gcur, tile);
   }
   for (; tile < p.num_tiles; tile += NSLOT * G) {
@@ -122,8 +134,13 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
     for (int l = p.L; l >= 1; --l) {
       uint32_t v[32];
       uint8_t* drow = p.d_img[l - 1] + tile * img_tile_bytes(W);
-      if (l > 1) load_h(hnext, l - 1, tile);
-      else if (next < p.num_tiles) load_h(hnext, p.L, next);
+      if (BITS) {
+        if (l > 1) load_m(mnext, l - 1, tile);
+        else if (next < p.num_tiles) load_m(mnext, p.L, next);
+      } else {
+        if (l > 1) load_h(hnext, l - 1, tile);
+        else if (next < p.num_tiles) load_h(hnext, p.L, next);
+      }
       if (l < p.L) {
         mbar_wait(acc_full, ph);
         ph ^= 1u;
@@ -145,22 +162,29 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
           g[i] = d;
         }
         uint32_t pk[16];
+        if (BITS) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 hv = hcur[4 * c + q];
-          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+          for (int j = 0; j < 16; ++j)
+            pk[j] = pack_bf16x2(((mcur[c] >> (2 * j)) & 1u) ? g[2 * j] : 0.f,
+                                ((mcur[c] >> (2 * j + 1)) & 1u) ? g[2 * j + 1] : 0.f);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int i = 8 * q + 2 * e;
-            float m0, m1;
-            if (p.sine) {  // g * cos(z_l)
-              m0 = g[i] * __uint_as_float(hw[e] << 16);
-              m1 = g[i + 1] * __uint_as_float(hw[e] & 0xFFFF0000u);
-            } else {
-              m0 = (hw[e] & 0x7FFFu) ? g[i] : 0.f;           // h > 0 (h >= 0 by ReLU)
-              m1 = (hw[e] & 0x7FFF0000u) ? g[i + 1] : 0.f;
+          for (int q = 0; q < 4; ++q) {
+            const uint4 hv = hcur[4 * c + q];
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 8 * q + 2 * e;
+              float m0, m1;
+              if (p.sine) {  // g * cos(z_l)
+                m0 = g[i] * __uint_as_float(hw[e] << 16);
+                m1 = g[i + 1] * __uint_as_float(hw[e] & 0xFFFF0000u);
+              } else {
+                m0 = (hw[e] & 0x7FFFu) ? g[i] : 0.f;           // h > 0 (h >= 0 by ReLU)
+                m1 = (hw[e] & 0x7FFF0000u) ? g[i + 1] : 0.f;
+              }
+              pk[4 * q + e] = pack_bf16x2(m0, m1);
             }
-            pk[4 * q + e] = pack_bf16x2(m0, m1);
           }
         }
 #pragma unroll
@@ -169,8 +193,13 @@ __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         if (l >= 2) tmem_st16(trow + acol + 16u * c, pk);
       }
+      if (BITS) {
 #pragma unroll
-      for (int q = 0; q < HW; ++q) hcur[q] = hnext[q];
+        for (int q = 0; q < MW; ++q) mcur[q] = mnext[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < HW; ++q) hcur[q] = hnext[q];
+      }
       if (l >= 2) {
         // delta_l is in TMEM: MMA dL/dh_{l-1} = delta_l W_l (K = out of layer l)
         tmem_wait_st();
@@ -229,8 +258,20 @@ struct DwJob {
 constexpr int kMaxDwJobs = 2 * kMaxLayers + 3;
 constexpr int kDwCols = kDwMaxN + 16;  // partial columns per CTA (features + ones block)
 // partial of CTA c of job j, column col, D row m: [(j * cpj + c) * kDwCols + col] * 128 + m
+// Adam + bf16 re-pack fused into k_dw_reduce (no communicator: the reduced
+// gradient is final, so the thread that writes g_i also steps parameter i).
+struct AdamFuse {
+  int on;
+  float* th;
+  float* m;
+  float* v;
+  const float* grad;  // gradient blob base (w_out / b_out point into it)
+  AdamArgs h;
+  PackArgs a;
+};
 struct DwJobs {
   DwJob job[kMaxDwJobs];
+  AdamFuse adam;
   int njobs, cpj;
   int nst;        // TMA pipeline stages (<= kDwMaxStages)
   int accumulate; // add into the partials (micro-batches after the first)
@@ -392,19 +433,21 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
 //   kind 0: hidden layer l >= 2: W[m][k] <- D[m][k], b[m] <- D[m][fb]
 //   kind 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
 //   kind 2: head row `row` of the head-gradient image: v[j] <- D[row][j], c <- D[row][fb]
-// Block = 32 consecutive output elements x 8 slices of the CTA range: thread
-// (e, s) sums CTAs [s * per, (s + 1) * per) in order, then slice 0 adds the 8
-// slice sums in order — a fixed tree, so the result is deterministic.
-constexpr int kRedSlices = 8;
+// Block = 32 consecutive output elements x S slices of the CTA range (S fixed
+// by the CTA count: <= 8 partials per slice): thread (e, s) sums CTAs
+// [s * per, (s + 1) * per) in order (its loads in flight at once), then slice
+// 0 adds the S slice sums in order — a fixed tree, so the result is
+// deterministic.  With js.adam.on, that
+// thread also takes parameter i's Adam step and re-pack (nb_adam.cuh).
+constexpr int kRedSlices = 16;
 __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_constant__ DwJobs js) {
   __shared__ float part[kRedSlices][32];
-  const int e_in = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  int64_t e = (int64_t)blockIdx.x * 32 + e_in;  // global element index over all jobs
+  const int e_in = threadIdx.x & 31, sl = threadIdx.x >> 5, S = blockDim.x >> 5;
+  int e = blockIdx.x * 32 + e_in;  // global element index over all jobs (< 2^31)
   int jj = 0;
-  int64_t total = 0;
   for (; jj < js.njobs; ++jj) {
     const DwJob& r = js.job[jj];
-    total = (int64_t)(r.kind == 2 ? 1 : r.rows) * (r.in + 1);
+    const int total = (r.kind == 2 ? 1 : r.rows) * (r.in + 1);
     if (e < total) break;
     e -= total;
   }
@@ -413,25 +456,25 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
   int k = 0, m = 0;
   if (active) {
     const DwJob& r = js.job[jj];
-    const int rows = r.kind == 2 ? 1 : r.rows;
-    k = (int)(e / rows);                          // output column (k == in: bias)
-    m = r.kind == 2 ? r.row : (int)(e % rows);    // row of D
+    const unsigned rows = r.kind == 2 ? 1u : (unsigned)r.rows;
+    k = (int)((unsigned)e / rows);                        // output column (k == in: bias)
+    m = r.kind == 2 ? r.row : (int)((unsigned)e % rows);  // row of D
     const int c0 = k == r.in ? r.fb : k;
     const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : ((k != r.in && r.kind == 3) ? 32 + k : -1);
     const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
     const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
-    const int per = (js.cpj + kRedSlices - 1) / kRedSlices;
+    const int per = (js.cpj + S - 1) / S;
     const int cb = sl * per, ce = min(js.cpj, cb + per);
-    for (int c = cb; c < ce; c += 8) {
-      float x0[8], x1[8];
+    for (int c = cb; c < ce; c += 16) {
+      float x0[16], x1[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const bool ok = c + u < ce;
         x0[u] = ok ? __ldg(P + (c + u) * cs + (int64_t)c0 * 128) : 0.f;
         x1[u] = (ok && c1 >= 0) ? __ldg(P + (c + u) * cs + (int64_t)c1 * 128) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         if (c + u < ce) {
           acc += x0[u];
           if (c1 >= 0) acc += x1[u];
@@ -443,17 +486,18 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
   __syncthreads();
   if (sl == 0 && active) {
     float t = 0.f;
-#pragma unroll
-    for (int q = 0; q < kRedSlices; ++q) t += part[q][e_in];
+    for (int q = 0; q < S; ++q) t += part[q][e_in];
     const DwJob& r = js.job[jj];
+    float* out;
     if (r.kind == 2) {
-      if (k == r.in) *r.b_out = t;
-      else r.w_out[k] = t;
+      out = k == r.in ? r.b_out : r.w_out + k;
     } else {
       const int mo = m + r.m_off;
-      if (k == r.in) r.b_out[mo] = t;
-      else r.w_out[(int64_t)mo * r.in + k] = t;
+      out = k == r.in ? r.b_out + mo : r.w_out + (int64_t)mo * r.in + k;
     }
+    *out = t;
+    if (js.adam.on)
+      adam_pack_one(out - js.adam.grad, t, js.adam.th, js.adam.m, js.adam.v, js.adam.h, js.adam.a);
   }
 }
 
@@ -463,7 +507,9 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
     const DwJob& r = js.job[jj];
     total += (int64_t)(r.kind == 2 ? 1 : r.rows) * (r.in + 1);
   }
-  k_dw_reduce<<<(unsigned)((total + 31) / 32), 32 * kRedSlices, 0, st>>>(js);
+  // slices of <= 8 CTA partials each (one round of loads), at most kRedSlices
+  const int S = std::max(1, std::min(kRedSlices, (js.cpj + 7) / 8));
+  k_dw_reduce<<<(unsigned)((total + 31) / 32), 32 * S, 0, st>>>(js);
   return cudaGetLastError();
 }
 
@@ -494,9 +540,10 @@ static TrainLayout train_layout(const nb_model* m, int64_t n, int grid) {
   t.x_img = take(T * img_tile_bytes((int)m->pl.k_of[0]));
   for (int l = 0; l < L; ++l) t.h_img[l] = take(T * img_tile_bytes(W));
   const bool sine = m->d.activation == NB_SINE;
-  // sine nets: cos(z_l) images; w = 256 ReLU (CTA pairs): the backward's bit masks
-  const bool masks = !sine && m->pl.pairs == 2 && m->d.n_heads == 0;
-  for (int l = 0; l < L; ++l) t.c_img[l] = sine ? take(T * img_tile_bytes(W)) : (masks ? take(T * 4096) : 0);
+  // sine nets: cos(z_l) images; ReLU nets: the backward's h_l > 0 bit masks
+  // (W / 32 words per row, W * 16 B per row tile; the CTA-pair path without heads)
+  const bool masks = !sine && !(m->pl.pairs == 2 && m->d.n_heads > 0) && !getenv("NB_NO_MASKS");
+  for (int l = 0; l < L; ++l) t.c_img[l] = sine ? take(T * img_tile_bytes(W)) : (masks ? take(T * W * 16) : 0);
   for (int l = 0; l < L; ++l) t.d_img[l] = take(T * img_tile_bytes(W));
   // the dW GEMM reads 128 features of A per tile: pad the last tile's images
   take(img_tile_bytes(128));
@@ -519,10 +566,11 @@ template <int W>
 static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) {
   size_t smem = ((m->pl.core_bytes + 15) & ~15u) + 64;
   smem = std::max<size_t>(smem, 116 * 1024);
-  cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = p.m_img[0] ? k_bwd_tc<W, true> : k_bwd_tc<W, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
-  k_bwd_tc<W><<<grid, 2 * 4 * 32, smem, st>>>(p);
+  kern<<<grid, 2 * 4 * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -559,7 +607,7 @@ cudaError_t launch_fwd_tc2(const nb_model* m, int mode, const FwdArgs& a, cudaSt
 bool train_fused_supported(const nb_model* m);
 cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, int64_t n,
                                int64_t n_global, float alpha, float beta, float* partial,
-                               int* cpj, cudaStream_t st);
+                               int* cpj, int* head_row, cudaStream_t st);
 
 // One micro-batch: forward (kTrain) + backward chain + dW GEMMs (partials
 // written when `first`, accumulated otherwise).
@@ -608,6 +656,8 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
     bp.d_img[l] = base + tl.d_img[l];
     bp.c_img[l] = sine ? base + tl.c_img[l] : nullptr;
   }
+  for (int l = 0; l < kMaxLayers; ++l)
+    bp.m_img[l] = (!sine && l < L && tl.c_img[l]) ? reinterpret_cast<const uint32_t*>(base + tl.c_img[l]) : nullptr;
   bp.sine = sine ? 1 : 0;
   bp.g32 = (float*)(base + tl.g32);
   if (pairs)
@@ -625,22 +675,33 @@ static cudaError_t train_chunk(nb_model* m, const float* q, const uint8_t* y, in
 }
 
 cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64_t n,
-                            int64_t n_global, float alpha, float beta, cudaStream_t st) {
+                            int64_t n_global, float alpha, float beta, float fuse_lr, cudaStream_t st) {
   const int W = m->d.width, L = m->d.hidden_layers, d0 = m->d0;
+  AdamFuse af{};
+  if (fuse_lr > 0.f) {
+    af.on = 1;
+    af.th = m->theta;
+    af.m = m->adam_m;
+    af.v = m->adam_v;
+    af.grad = m->grad;
+    adam_setup(m, fuse_lr, &af.h, &af.a);
+  }
   const int64_t chunk = train_chunk_rows(m, n);
   TrainLayout tl = train_layout(m, chunk, m->num_sms);
   uint8_t* base = (uint8_t*)m->train_scratch;
   if (n > 0 && n <= chunk && train_fused_supported(m) && !getenv("NB_NO_FUSED")) {
     // w = 64: forward + loss + backward + dW in one kernel (nb_train_fused.cu)
     DwJobs fj{};
+    fj.adam = af;
     fj.partial = (float*)(base + tl.partial);
     float* g = m->grad;
     fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, 16, 1, W, 0, d0, d0, g + m->po.W[0], g + m->po.b[0]};
     for (int l = 1; l < L; ++l)
       fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 0, W, 0, d0, W, g + m->po.W[l], g + m->po.b[l]};
-    // the head gradient rides in row 64 of the last layer's delta image
-    fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
-    cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, st);
+    // the head gradient: D row head_row (set by the kernel choice)
+    DwJob& hj = fj.job[fj.njobs++];
+    hj = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
+    cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, &hj.row, st);
     if (e != cudaSuccess) return e;
     return launch_dw_reduce(fj, st);
   }
@@ -680,7 +741,8 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     e = train_chunk(m, q + c0 * d0, y + c0, rows, n_global, alpha, beta, c0 == 0, js, tl, st);
   }
   if (e != cudaSuccess) return e;
-  // 4. fixed-order reduction of all partials into the gradient blob
+  // 4. fixed-order reduction of all partials into the gradient blob (+ Adam)
+  js.adam = af;
   return launch_dw_reduce(js, st);
 }
 

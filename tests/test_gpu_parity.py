@@ -440,6 +440,33 @@ def test_train_micro_batches_equal_one_batch(name, monkeypatch):
     assert np.linalg.norm(g1 - g2) <= 1e-5 * np.linalg.norm(g1)
 
 
+@pytest.mark.parametrize("name,fused", [("c2", False), ("c3", True), ("c4", True), ("c5", True)])
+def test_relu_bit_masks_equal_h_images(name, fused, monkeypatch):
+    """The backward's ReLU' (R25: [h_l > 0]) read from the forward's bit masks
+    equals the one read from the h_l images: bit-identical gradient, loss and
+    counts (NB_NO_MASKS=1 selects the h-image read; c2 runs the unfused
+    kernels with NB_NO_FUSED=1)."""
+    cfg = nbgen.CONFIGS[name]
+    n = 7 * 1024 + 77
+    q = nbgen.make_queries(cfg, nbgen.TAG_TRAIN, 0, n)
+    y = labels_oracle(cfg, q.numpy())
+    th = scaled_params(cfg, 13)
+    if not fused:
+        monkeypatch.setenv("NB_NO_FUSED", "1")
+    out = []
+    for no_masks in (False, True):
+        if no_masks:
+            monkeypatch.setenv("NB_NO_MASKS", "1")
+        m = nb.Model(desc_of(cfg), DEV)
+        m.set_params(th)
+        st = m.train_step(cuda(q), cuda(y), alpha=20.0, beta=1.0, lr=1e-3, stats=True)
+        out.append((st, m.get_grad()))
+    (s1, g1), (s2, g2) = out
+    assert all(s1[k] == s2[k] for k in ("tp", "fp", "fn", "tn")), (s1, s2)
+    assert abs(s1["loss"] - s2["loss"]) <= 1e-12 * abs(s1["loss"])   # fp64 atomic sum order
+    assert torch.equal(g1, g2), float((g1 - g2).abs().max())
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c5"])
 def test_nonfinite_records(name):
     """Non-finite input ("non-finite input -> error"; R26):
