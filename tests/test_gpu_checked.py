@@ -79,8 +79,8 @@ def test_output_guard_regions_untouched(name, n):
     y = (q[:, 0] < 0.5).to(torch.uint8)
     G = 4096
     nl = 1 + cfg.n_heads
-    logits = torch.full((n * nl + G,), 7.25, device="cuda:0")
-    prob = torch.full((n + G,), 7.25, device="cuda:0")
+    logits = torch.full((n * nl + G,), 7.25, dtype=torch.float32, device="cuda:0")
+    prob = torch.full((n + G,), 7.25, dtype=torch.float32, device="cuda:0")
     st = torch.cuda.current_stream().cuda_stream
     L = nb.lib()
     assert L.nb_forward(m._h, q.data_ptr(), n, logits.data_ptr(), prob.data_ptr(), st) == 0

@@ -12,7 +12,17 @@ import torch
 
 import oracle
 
-torch.set_default_dtype(torch.float64)
+
+
+@pytest.fixture(autouse=True)
+def _float64_default():
+    """fp64 torch references inside this module only: a module-level
+    set_default_dtype leaked into every later test of the session (a GPU
+    test's torch.full output buffers became float64)."""
+    prev = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(prev)
 
 
 def torch_features(x, pe):
