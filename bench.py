@@ -110,6 +110,16 @@ def load_peaks():
     return 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def load_sustained_peak():
+    """the driver's sustained bf16 figure (cuBLAS back to back for 4 s): context
+    for a kernel timed over seconds under the board power cap; the line's
+    `frac` stays against the burst peak (the conservative denominator)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("bf16_tflops_sustained")
+    return None
+
+
 def load_traffic():
     """dram bytes per launch of the score kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -433,7 +443,9 @@ def run_ours(args):
                          "kernel": KERNEL[CONFIG],
                          "flop_per_query": exit_info["executed_flop_per_query"] if exit_info else fq,
                          "kernel_ms_per_launch": per_launch_ms,
-                         "ncu_tensor_pipe_pct": tensor_pct},
+                         "ncu_tensor_pipe_pct": tensor_pct,
+                         "peak_sustained": load_sustained_peak(),
+                         "frac_vs_sustained": (achieved / load_sustained_peak()) if load_sustained_peak() else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (4 * cfg.record_floats + 1),
                     "d2h_bytes_per_step": 9 * 8, "api": "nb_score_host (pinned host q/y)",
                     "bytes": "per rank"},

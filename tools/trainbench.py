@@ -12,6 +12,9 @@ import torch
 import nbgen
 import paper_2310_06822_b200 as nb
 
+if os.environ.get("NB_LIB", ""):  # measurement variant (build.py name=...)
+    nb.LIB_PATH = os.path.join(os.path.dirname(nb.LIB_PATH), f"libnb_{os.environ['NB_LIB']}.so")
+
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 cfg = nbgen.CONFIGS[name]
