@@ -391,12 +391,31 @@ def run_ours(args):
         nb.lib().nb_debug_set_dense_exits(0)
         assert m.counts_dict(out[0]) == c
         dense_ms = sorted(dts)[len(dts) // 2]
+        # the record hand-off between the segments (8x less DRAM, recomputes)
+        nb.lib().nb_debug_set_exit_records(1)
+        for i in range(3):
+            step(i)
+        torch.cuda.synchronize()
+        rts = []
+        for i in range(min(args.steps, 10)):
+            flush.fill_(i & 0xFF)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            step(i)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            rts.append(a0.elapsed_time(a1))
+        nb.lib().nb_debug_set_exit_records(0)
+        assert m.counts_dict(out[0]) == c
+        rec_ms = sorted(rts)[len(rts) // 2]
         exit_info = {"exit_hist": c["exit_hist"], "bins": "exit@1, exit@2, final-negative, final-positive",
                      "survive_head1": (n_total - c["exit_hist"][0]) / n_total,
                      "survive_head2": (n_total - c["exit_hist"][0] - c["exit_hist"][1]) / n_total,
                      "executed_flop_per_query": fq_exec, "dense_flop_per_query": fq,
                      "dense_kernel_q_per_s": n_total / (dense_ms * 1e-3),
                      "dense_kernel_ms_per_step": dense_ms,
+                     "records_handoff_q_per_s": n_total / (rec_ms * 1e-3),
+                     "records_handoff_ms_per_step": rec_ms,
                      "model": f"trained {args.model_train_steps} Adam steps (Eq. 1, alpha 1->1000) "
                               "from Xavier init, calibrated to FN = 0 on the step's queries"}
     else:

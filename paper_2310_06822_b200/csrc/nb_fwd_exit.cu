@@ -50,13 +50,15 @@ struct ExitParams {
   float tau_end;             // threshold of the head ending the segment / output
   uint32_t hc_off;           // packed offset of that head's fp32 constant (c_k / b_out)
   // weights: up to 2 * SEG + 1 bulk copies packed -> shared memory
-  uint32_t cp_src[8], cp_dst[8], cp_len[8];
+  uint32_t cp_src[16], cp_dst[16], cp_len[16];
   int ncp;
   uint32_t wbytes;           // bytes of the shared weight area
-  uint32_t s_w[4], s_bb[4];  // shared offsets of the segment's layer images / bias blocks
+  uint32_t s_w[8], s_bb[8];  // shared offsets of the segment's layer images / bias blocks
   uint32_t s_head;           // head vector (W floats: u_k / w_out)
   // regions (R = kXSlots * gridDim.x)
   const uint8_t* in_img;
+  const float* in_rec;       // IN = 2: survivors' records of the previous segment (regions)
+  float* out_rec;            // REC: survivors' records appended to this slot's region
   const uint8_t* in_lab;
   const uint32_t* in_cnt;
   uint8_t* out_img;
@@ -94,11 +96,16 @@ __device__ __forceinline__ void st_img_row(uint8_t* tile, int row, int fg0, cons
         make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
 }
 
-// SEG hidden layers [lb, lb + SEG); IN_IMG: input is the previous segment's
-// image regions (else fp32 records); HEAD = exit head ending the segment
-// (0, 1), or -1: the segment ends with the output layer and classifies.
-template <int SEG, bool IN_IMG, int HEAD, int D0C>
+// SEG hidden layers [lb, lb + SEG); IN = 0: the caller's fp32 records,
+// 1: the previous segment's image regions, 2: the previous segment's record
+// regions (the segment then starts at layer 0 and recomputes the layers
+// before it); HEAD = exit head ending the segment (0, 1), or -1: the segment
+// ends with the output layer and classifies.  REC: survivors hand their
+// fp32 record (d0 floats, 16 B for c4) to the next segment instead of their
+// bf16 activations (256 B).
+template <int SEG, int IN, int HEAD, int D0C, bool REC = false>
 __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams p) {
+  constexpr bool IN_IMG = IN == 1, IN_REG = IN != 0;  // input from regions (prefix-summed tiles)
   constexpr int W = kXW, NSLOT = kXSlots, WPS = kXWps, NEPI = kXWarps;
   constexpr int CPT = W * 4 / WPS, NCH = CPT / 32;  // 64 columns per thread
   constexpr bool FINAL = HEAD < 0;
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
   for (int i = threadIdx.x; i < NEPI * 12; i += blockDim.x) ctr[i] = 0u;
   // tiles of this segment: regions' tile counts, exclusive prefix in pref[0..R]
   int64_t num_tiles = p.num_tiles;
-  if (IN_IMG) {
+  if (IN_REG) {
     uint32_t c = 0;
     if ((int)threadIdx.x < R) {
       const uint32_t rc = __ldg(p.in_cnt + threadIdx.x);
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (IN_IMG) num_tiles = pref[R];
+  if (IN_REG) num_tiles = pref[R];
   const uint32_t tmem = *tmem_slot;
   NB_CHECK((tmem & 0xFFFFu) == 0u);  // the whole allocation starts at column 0
   {  // ones block (bias folding): k = 0, 1, 2 of every row are 1.0
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
 
   // input tile t -> (region, tile in region, valid rows)
   auto locate = [&](int64_t t, int& r, int& j, int& rows) {
-    if (!IN_IMG) {
+    if (!IN_REG) {
       r = 0; j = 0;
       rows = (int)min((int64_t)kTile, p.a.n - t * kTile);
       return;
@@ -261,6 +268,14 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
       mbar_arrive_expect_tx(bar, kImgTile + (uint32_t)kTile);
       bulk_g2s(smem_u32(stage_ptr(s, b)), p.in_img + ti * kImgTile, kImgTile, bar);
       bulk_g2s(smem_u32(lab_ptr(s, b)), p.in_lab + ti * kTile, kTile, bar);
+    } else if (IN == 2) {  // a whole region tile (rows past the region count are masked)
+      int r, j, rows;
+      locate(t, r, j, rows);
+      const int64_t ti = (int64_t)r * p.cap + j;
+      const uint32_t qb = (uint32_t)(kTile * d0 * 4);
+      mbar_arrive_expect_tx(bar, qb + (uint32_t)kTile);
+      bulk_g2s(smem_u32(stage_ptr(s, b)), p.in_rec + ti * kTile * d0, qb, bar);
+      bulk_g2s(smem_u32(lab_ptr(s, b)), p.in_lab + ti * kTile, kTile, bar);
     } else {
       if ((t + 1) * kTile > p.a.n) return;  // ragged last tile: read directly
       const uint32_t qb = (uint32_t)(kTile * d0 * 4);
@@ -273,6 +288,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
   uint32_t sph[2] = {0u, 0u};
   int ycur = 0;      // lead threads: label byte of the staged row (bit 0 y, bit 1 counted non-finite)
   bool vcur = false;
+  const float* srccur = nullptr;  // REC: the staged row's record in global memory (lead threads)
   auto put_input = [&](int64_t t, int i) {
     const int b = i & 1;
     int r, j, rows;
@@ -289,9 +305,11 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
     }
     if (lead) {
       float x[8];
-      const bool full = (t + 1) * kTile <= p.a.n;
+      const bool full = IN == 2 || (t + 1) * kTile <= p.a.n;
       vcur = rit < rows;
       int yv;
+      if (IN == 2) srccur = p.in_rec + (((int64_t)r * p.cap + j) * kTile + rit) * d0;
+      else srccur = p.a.q + (t * kTile + rit) * d0;
       if (full) {
         mbar_wait(stage_bar(s, b), sph[b]);
         sph[b] ^= 1u;
@@ -305,8 +323,12 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
         for (int jj = 0; jj < 8; ++jj) x[jj] = (vcur && jj < d0) ? __ldg(p.a.q + rr * d0 + jj) : 0.f;
         yv = vcur ? (int)__ldg(p.a.y + rr) : 0;
       }
-      if (vcur && yv > 1) atomicOr(p.a.flags, kFlagLabel);
-      ycur = yv != 0 ? 1 : 0;
+      if (IN == 2) {
+        ycur = yv;  // bit 0 y, bit 1 non-finite already counted (set by an earlier segment)
+      } else {
+        if (vcur && yv > 1) atomicOr(p.a.flags, kFlagLabel);
+        ycur = yv != 0 ? 1 : 0;
+      }
       uint32_t c[8];
       encode_cols<D0C, true>(x, d0, c);
       tmem_st8(trow + enc_c, c);
@@ -327,6 +349,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
     const int64_t next = tile + NSLOT * G;
     int ythis = 0;
     bool vthis = false;
+    const float* srcthis = nullptr;
     float za = lead ? hconst : 0.f, zb = 0.f;
 #pragma unroll
     for (int li = 0; li < SEG; ++li) {
@@ -343,6 +366,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
       if (last) {  // accumulator in registers: start the slot's next tile
         ythis = ycur;
         vthis = vcur;
+        srcthis = srccur;
         ++i_tile;
         if (next < num_tiles) put_input(next, i_tile);
       }
@@ -429,10 +453,17 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
         if (surv) {
           pos = (int)(out_base + below + __popc(bs & ((1u << lane) - 1u)));
           p.out_lab[(int64_t)region * p.cap * kTile + pos] = (uint8_t)((yy ? 1 : 0) | ((nf || nf_done) ? 2 : 0));
+          if (REC) {  // the row's record (16 B for c4): the next segment recomputes from it
+            float* o = p.out_rec + ((int64_t)region * p.cap * kTile + pos) * d0;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (jj < d0) o[jj] = __ldg(srcthis + jj);
+          }
         }
         out_base += tot;
         xpos[((s * 2 + par) * 4 + qw) * 32 + lane] = pos;
       }
+      if (!REC) {
       asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");
       if (!lead) pos = xpos[((s * 2 + par) * 4 + qw) * 32 + lane];
 #ifndef NB_EXIT_NOSTORE
@@ -444,6 +475,7 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
         st_img_row(ot, pos & (kTile - 1), col0 / 8, w);
       }
 #endif
+      }
     }
     par ^= 1u;
     tile = next;
@@ -459,11 +491,12 @@ __global__ void __launch_bounds__(kXWarps * 32, 1) k_score_exit(const ExitParams
   if (warp == 1 && p.a.ticket) finalize_counts(p.a, false);
 }
 
-template <int SEG, bool IN_IMG, int HEAD, int D0C>
+template <int SEG, int IN, int HEAD, int D0C, bool REC = false>
 cudaError_t launch_seg(const nb_model* m, ExitParams p, cudaStream_t st) {
-  const ExitSmem L(p.wbytes, IN_IMG);
+  const ExitSmem L(p.wbytes, IN == 1);
   const size_t smem = std::max<size_t>(L.total, 116 * 1024);
-  auto kern = k_score_exit<SEG, IN_IMG, HEAD, D0C>;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto kern = k_score_exit<SEG, IN, HEAD, D0C, REC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<m->num_sms, kXWarps * 32, smem, st>>>(p);
@@ -511,9 +544,18 @@ bool exit_compaction_supported(const nb_model* m) {
 // launches add to a.counts; the last one finalises into a.fin_out.
 static int64_t g_exit_chunk = 0;  // rows per chunk override (tests), 0 = default
 extern "C" void nb_debug_set_exit_chunk(int64_t rows) { g_exit_chunk = rows; }
+static int g_exit_records = 0;    // record hand-off instead of activation images
+extern "C" void nb_debug_set_exit_records(int on) { g_exit_records = on ? 1 : 0; }
 
 cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st, int* kernels) {
   *kernels = 0;
+  // hand-off between segments: the survivors' bf16 activation images (256 B
+  // per c4 row; default, the faster one) or their fp32 records (16 B; the
+  // later segments recompute the earlier layers: 8x less DRAM traffic, ~7 %
+  // slower on a trained c4 model) — nb_debug_set_exit_records
+  // or NB_EXIT_RECORDS=1
+  static const bool env_records = getenv("NB_EXIT_RECORDS") != nullptr;
+  const bool images = !(env_records || g_exit_records);
   static const int64_t env_chunk = [] {
     const char* e = getenv("NB_EXIT_CHUNK");
     return e ? atoll(e) : (int64_t)1 << 24;
@@ -521,9 +563,11 @@ cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st, in
   const int64_t want = std::max<int64_t>(kTile, (g_exit_chunk > 0 ? g_exit_chunk : env_chunk) / kTile * kTile);
   const int64_t chunk = std::min<int64_t>(want, (a.n + kTile - 1) / kTile * kTile);
   const int R = m->num_sms * kXSlots;
+  const int d0 = m->d0;
   const int64_t t0 = (chunk + kTile - 1) / kTile;
   const int64_t cap = (t0 + R + R - 1) / R;
-  const size_t img_bytes = (size_t)R * cap * kImgTile, lab_bytes = (size_t)R * cap * kTile;
+  const size_t row_bytes = images ? (size_t)kImgTile : (size_t)kTile * d0 * 4;  // per region tile
+  const size_t img_bytes = (size_t)R * cap * row_bytes, lab_bytes = (size_t)R * cap * kTile;
   const size_t need = 2 * (img_bytes + lab_bytes) + 2 * 4 * (size_t)R;
   if (m->exit_scratch_bytes < need) {
     cudaFree(m->exit_scratch);
@@ -538,7 +582,7 @@ cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st, in
   uint8_t* lab[2] = {base + 2 * img_bytes, base + 2 * img_bytes + lab_bytes};
   uint32_t* cnt[2] = {(uint32_t*)(base + 2 * (img_bytes + lab_bytes)),
                       (uint32_t*)(base + 2 * (img_bytes + lab_bytes)) + R};
-  const int h0 = m->d.head_after[0], h1 = m->d.head_after[1];
+  const int h0 = m->d.head_after[0], h1 = m->d.head_after[1], L = m->d.hidden_layers;
   for (int64_t r0 = 0; r0 < a.n; r0 += chunk) {
     const int64_t rows = std::min(chunk, a.n - r0);
     const bool last_chunk = r0 + rows >= a.n;
@@ -546,36 +590,59 @@ cudaError_t launch_score_exit(nb_model* m, const FwdArgs& a, cudaStream_t st, in
     p.a = a;
     p.a.ticket = nullptr;
     p.packed = m->packed;
-    p.d0 = m->d0;
+    p.d0 = d0;
     p.cap = cap;
     // segment 0: records -> layers [0, h0) -> head 1
-    p.a.q = a.q + r0 * m->d0;
+    p.a.q = a.q + r0 * d0;
     p.a.y = a.y + r0;
     p.a.n = rows;
     p.num_tiles = (rows + kTile - 1) / kTile;
     p.lb = 0;
     p.tau_end = a.tau[1];
     plan_weights(m, p, 0, h0, 0);
-    p.out_img = img[0]; p.out_lab = lab[0]; p.out_cnt = cnt[0];
-    cudaError_t e = m->d0 == 4 ? launch_seg<2, false, 0, 4>(m, p, st) : launch_seg<2, false, 0, 0>(m, p, st);
+    p.out_lab = lab[0]; p.out_cnt = cnt[0];
+    cudaError_t e;
+    if (images) {
+      p.out_img = img[0];
+      e = d0 == 4 ? launch_seg<2, 0, 0, 4>(m, p, st) : launch_seg<2, 0, 0, 0>(m, p, st);
+    } else {
+      p.out_rec = (float*)img[0];
+      e = d0 == 4 ? launch_seg<2, 0, 0, 4, true>(m, p, st) : launch_seg<2, 0, 0, 0, true>(m, p, st);
+    }
     if (e != cudaSuccess) return e;
     *kernels += 3;
-    // segment 1: image -> layers [h0, h1) -> head 2
-    p.lb = h0;
+    // segment 1: image -> layers [h0, h1) -> head 2, or records -> layers [0, h1) -> head 2
     p.tau_end = a.tau[2];
-    plan_weights(m, p, h0, h1 - h0, 1);
-    p.in_img = img[0]; p.in_lab = lab[0]; p.in_cnt = cnt[0];
-    p.out_img = img[1]; p.out_lab = lab[1]; p.out_cnt = cnt[1];
-    e = launch_seg<2, true, 1, 0>(m, p, st);
+    p.in_lab = lab[0]; p.in_cnt = cnt[0];
+    p.out_lab = lab[1]; p.out_cnt = cnt[1];
+    if (images) {
+      p.lb = h0;
+      plan_weights(m, p, h0, h1 - h0, 1);
+      p.in_img = img[0]; p.out_img = img[1];
+      e = launch_seg<2, 1, 1, 0>(m, p, st);
+    } else {
+      p.lb = 0;
+      plan_weights(m, p, 0, h1, 1);
+      p.in_rec = (const float*)img[0]; p.out_rec = (float*)img[1];
+      e = d0 == 4 ? launch_seg<4, 2, 1, 4, true>(m, p, st) : launch_seg<4, 2, 1, 0, true>(m, p, st);
+    }
     if (e != cudaSuccess) return e;
-    // segment 2: image -> layers [h1, L) -> output, classify
-    p.lb = h1;
+    // segment 2: image -> layers [h1, L) -> output, or records -> layers [0, L) -> output; classify
     p.tau_end = a.tau[0];
-    plan_weights(m, p, h1, m->d.hidden_layers - h1, -1);
-    p.in_img = img[1]; p.in_lab = lab[1]; p.in_cnt = cnt[1];
-    p.out_img = nullptr; p.out_lab = nullptr; p.out_cnt = nullptr;
+    p.in_lab = lab[1]; p.in_cnt = cnt[1];
+    p.out_img = nullptr; p.out_rec = nullptr; p.out_lab = nullptr; p.out_cnt = nullptr;
     if (last_chunk) p.a.ticket = a.ticket;
-    e = launch_seg<2, true, -1, 0>(m, p, st);
+    if (images) {
+      p.lb = h1;
+      plan_weights(m, p, h1, L - h1, -1);
+      p.in_img = img[1];
+      e = launch_seg<2, 1, -1, 0>(m, p, st);
+    } else {
+      p.lb = 0;
+      plan_weights(m, p, 0, L, -1);
+      p.in_rec = (const float*)img[1];
+      e = d0 == 4 ? launch_seg<6, 2, -1, 4>(m, p, st) : launch_seg<6, 2, -1, 0>(m, p, st);
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

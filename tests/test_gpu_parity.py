@@ -636,18 +636,35 @@ def _score_both(m, qd, yd):
     return c, d
 
 
+class _ExitRecords:
+    """Select the record hand-off between the exit segments (survivors' fp32
+    records, later segments recompute the earlier layers) for a block."""
+
+    def __init__(self, on):
+        self.on = on
+
+    def __enter__(self):
+        nb.lib().nb_debug_set_exit_records(1 if self.on else 0)
+
+    def __exit__(self, *a):
+        nb.lib().nb_debug_set_exit_records(0)
+
+
+@pytest.mark.parametrize("handoff", ["images", "records"])
 @pytest.mark.parametrize("n", [1, 127, 128, 129, 2 * 148 * 128 + 77, (1 << 20) + 5])
-def test_exit_compaction_counts_equal_dense(n):
+def test_exit_compaction_counts_equal_dense(n, handoff):
     """the compacted three-segment score (survivors of each head
     packed into full tiles) gives exactly the dense kernel's counts and exit
-    histogram; thresholds are set at logit quantiles so both heads exit a
-    sizeable share of rows."""
+    histogram, with either hand-off between the segments (activation images
+    or records + recompute); thresholds are set at logit quantiles so both
+    heads exit a sizeable share of rows."""
     cfg, q, y, m = _exit_model(n)
     qd, yd = cuda(q), cuda(y)
     z = m.forward(qd).cpu()
     m.set_thresholds([float(z[:, 0].median()), float(z[:, 1].quantile(0.4)) if n > 1 else 0.0,
                       float(z[:, 2].quantile(0.3)) if n > 1 else 0.0])
-    c, d = _score_both(m, qd, yd)
+    with _ExitRecords(handoff == "records"):
+        c, d = _score_both(m, qd, yd)
     assert c == d, (c, d)
     assert sum(c["exit_hist"]) == n
     if n > 1000:
@@ -670,11 +687,15 @@ def test_exit_compaction_vs_oracle_and_chunks():
     try:
         L.nb_debug_set_exit_chunk(1 << 20)
         c, d = _score_both(m, qd, yd)
+        with _ExitRecords(True):
+            cr, _ = _score_both(m, qd, yd)
         L.nb_debug_set_exit_chunk(0)
         c1, _ = _score_both(m, qd, yd)
+        with _ExitRecords(True):
+            cr1, _ = _score_both(m, qd, yd)
     finally:
         L.nb_debug_set_exit_chunk(0)
-    assert c == d and c1 == d
+    assert c == d and c1 == d and cr == d and cr1 == d
     # oracle on a sample of rows away from every threshold
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(n, 40000, replace=False))
