@@ -345,8 +345,12 @@ nb_status nb_model_create(const nb_desc* desc, int32_t device, nb_model** out) {
   A((void**)&m->d_counts, sizeof(unsigned long long) * 256);
   A((void**)&m->d_keys, sizeof(unsigned int) * 4);
   A((void**)&m->d_flags, sizeof(unsigned int) * 4);
-  A((void**)&m->d_loss, 64);  // [0, 16): loss (double), [16, 48): batch stats (4 x u64)
-  if (e == cudaSuccess) m->d_stats = reinterpret_cast<unsigned long long*>(m->d_loss + 2);
+  // two 64-B step-statistics buffers: [0, 16) loss (double), [16, 48) batch stats (4 x u64)
+  A((void**)&m->d_loss_base, 128);
+  if (e == cudaSuccess) {
+    m->d_loss = m->d_loss_base;
+    m->d_stats = reinterpret_cast<unsigned long long*>(m->d_loss + 2);
+  }
   if (e == cudaSuccess) e = cudaMallocHost((void**)&m->h_pinned, 256);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -384,7 +388,7 @@ void nb_model_destroy(nb_model* m) {
   cudaFree(m->d_counts);
   cudaFree(m->d_keys);
   cudaFree(m->d_flags);
-  cudaFree(m->d_loss);
+  cudaFree(m->d_loss_base);
   cudaFree(m->train_scratch);
   cudaFree(m->exit_scratch);
   cudaFree(m->hier_scratch);
@@ -778,7 +782,12 @@ static nb_status train_prepare(nb_model* m, const float* q, const uint8_t* y, in
 static nb_status train_enqueue(nb_model* m, const float* q, const uint8_t* y, int64_t n_local,
                                int64_t n_global, float alpha, float beta, float lr, cudaStream_t s) {
   const bool tc = m->d.precision == NB_BF16;
-  NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));  // loss and batch stats (one block)
+  // this step's statistics buffer; tensor-core steps find it zeroed by the
+  // previous step's gradient reduce (or by model creation)
+  m->d_loss = m->d_loss_base + 8 * m->lbuf;
+  m->d_stats = reinterpret_cast<unsigned long long*>(m->d_loss + 2);
+  m->lbuf ^= 1;
+  if (!tc) NB_CUDA(cudaMemsetAsync(m->d_loss, 0, 64, s));
   if (tc) {
     g_err.clear();
     // without a communicator the reduced gradient is final: Adam rides in the reduce

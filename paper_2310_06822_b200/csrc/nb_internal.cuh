@@ -101,8 +101,14 @@ struct nb_model {
   unsigned int* d_keys = nullptr;          // [3] order-preserving min keys
   unsigned int* d_flags = nullptr;         // sticky flags, [2], [3] score tickets
   int score_parity = 0;                    // counter set of the next score launch
-  double* d_loss = nullptr;                // [1]
-  unsigned long long* d_stats = nullptr;   // [4] batch tp fp fn tn
+  double* d_loss = nullptr;                // [1] loss of the current step's buffer
+  unsigned long long* d_stats = nullptr;   // [4] batch tp fp fn tn (current buffer)
+  // the step statistics are double-buffered (2 x 64 B at d_loss_base): a
+  // tensor-core step accumulates into buffer `lbuf` and its gradient reduce
+  // zeroes the other one for the next step, so no memset sits between the
+  // steps' kernels (programmatic dependent launch, nb_train_tc.cu)
+  double* d_loss_base = nullptr;
+  int lbuf = 0;
   unsigned long long* h_pinned = nullptr;  // pinned host mirror for small readbacks
   // training scratch (grown on demand outside the timed hot path)
   void* train_scratch = nullptr;

@@ -277,6 +277,7 @@ struct DwJobs {
   int accumulate; // add into the partials (micro-batches after the first)
   uint32_t stage; // bytes per stage (A 32 KB + B of the widest job + ones block)
   float* partial;
+  unsigned long long* zero_next;  // k_dw_reduce: the next step's statistics buffer (8 words) to zero
 };
 constexpr int kDwMaxStages = 6;
 
@@ -442,6 +443,10 @@ __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs
 constexpr int kRedSlices = 16;
 __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_constant__ DwJobs js) {
   __shared__ float part[kRedSlices][32];
+  // the next step's fused kernel is a programmatic dependent of this one: it
+  // may be scheduled now (it waits for this grid before touching memory)
+  griddep_launch_dependents();
+  if (blockIdx.x == 0 && threadIdx.x < 8 && js.zero_next) js.zero_next[threadIdx.x] = 0ull;
   const int e_in = threadIdx.x & 31, sl = threadIdx.x >> 5, S = blockDim.x >> 5;
   int e = blockIdx.x * 32 + e_in;  // global element index over all jobs (< 2^31)
   int jj = 0;
@@ -509,6 +514,9 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
   }
   // slices of <= 8 CTA partials each (one round of loads), at most kRedSlices
   const int S = std::max(1, std::min(kRedSlices, (js.cpj + 7) / 8));
+  // a plain launch: as a programmatic dependent of the fused step kernel its
+  // 400 CTAs, scheduled early, slowed that kernel's tail (c2 step 30.5 ->
+  // 35.9 us, measured); the next step's kernel is the programmatic one
   k_dw_reduce<<<(unsigned)((total + 31) / 32), 32 * S, 0, st>>>(js);
   return cudaGetLastError();
 }
@@ -693,6 +701,7 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     // w = 64: forward + loss + backward + dW in one kernel (nb_train_fused.cu)
     DwJobs fj{};
     fj.adam = af;
+    fj.zero_next = reinterpret_cast<unsigned long long*>(m->d_loss_base + 8 * m->lbuf);
     fj.partial = (float*)(base + tl.partial);
     float* g = m->grad;
     fj.job[fj.njobs++] = DwJob{nullptr, W, 0, nullptr, 16, 1, W, 0, d0, d0, g + m->po.W[0], g + m->po.b[0]};
@@ -743,6 +752,7 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
   if (e != cudaSuccess) return e;
   // 4. fixed-order reduction of all partials into the gradient blob (+ Adam)
   js.adam = af;
+  js.zero_next = reinterpret_cast<unsigned long long*>(m->d_loss_base + 8 * m->lbuf);
   return launch_dw_reduce(js, st);
 }
 
