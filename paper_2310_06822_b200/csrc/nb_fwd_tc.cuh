@@ -357,8 +357,6 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     __syncthreads();
     tc_fence_after();
   }
-  mbar_wait(smem_u32(bars), 0);
-
   const bool dyn_n = MODE == kForward && p.a.n_dev;  // device-side row count (hierarchies)
   const int64_t n = dyn_n ? (int64_t)*p.a.n_dev : p.a.n;
   const int64_t num_tiles = dyn_n ? (n + kTile - 1) / kTile : p.num_tiles;
@@ -375,7 +373,7 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   const uint32_t trow = tmem + ((uint32_t)(qw * 32) << 16);
   const float* bias_all = reinterpret_cast<const float*>(smem + p.pl.off_bias);
   const float* wout = reinterpret_cast<const float*>(smem + p.pl.off_wout) + col0;
-  const float bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
+  float bout = 0.f;  // read once the weights are resident (below)
   const float* cst = reinterpret_cast<const float*>(smem + p.pl.off_c);
   const float* u0 = reinterpret_cast<const float*>(smem + p.pl.off_u[0]) + col0;
   const float* u1 = reinterpret_cast<const float*>(smem + p.pl.off_u[1]) + col0;
@@ -502,8 +500,12 @@ __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
   };
 
   int64_t tile = blockIdx.x + (int64_t)s * G;
+  // the slot's first two record tiles are requested before waiting for the
+  // weights, so the two HBM latencies overlap instead of adding up
   stage_issue(tile, 0);
   stage_issue(tile + NSLOT * G, 1);
+  mbar_wait(smem_u32(bars), 0);
+  bout = *reinterpret_cast<const float*>(smem + p.pl.off_bout);
   int i_tile = 0;
   if (tile < num_tiles) put_input(tile, 0);
   uint32_t par = 0;
