@@ -515,6 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   const uint32_t bar_off = (p.pl.bytes + 15u) & ~15u;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + bar_off);
   // [0] weights  [1] acc_a  [2] acc_b  [3] a_done (leader)  [4] b_done (leader)  [5,6] stage
+  // [11] b_done1 (leader): the second half of every warp's D_b columns (split signal)
   // [7,8] xfull  [9,10] xfree
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   float* xch = reinterpret_cast<float*>(tmem_slot + 4);                   // [2][4 groups][128]
@@ -528,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   // rows for all 128 rows of the tile
   uint8_t* ones = smem + (((uint32_t)(ylab + 2 * kTile - smem) + 127u) & ~127u);  // [L - 1][256 B]
   const uint32_t w_bar = smem_u32(bars), acc_a = smem_u32(bars + 1), acc_b = smem_u32(bars + 2);
-  const uint32_t a_done = smem_u32(bars + 3), b_done = smem_u32(bars + 4);
+  const uint32_t a_done = smem_u32(bars + 3), b_done = smem_u32(bars + 4), b_done1 = smem_u32(bars + 11);
   auto stage_bar = [&](int b) { return smem_u32(bars + 5 + b); };
   auto xfull = [&](int b) { return smem_u32(bars + 7 + b); };
   auto xfree = [&](int b) { return smem_u32(bars + 9 + b); };
@@ -541,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
       mbar_init(acc_b, 1);
       mbar_init(a_done, 2 * NEPI);  // one arrive per epilogue warp of both CTAs
       mbar_init(b_done, 2 * NEPI);
+      mbar_init(b_done1, 2 * NEPI);
       mbar_init(stage_bar(0), 1);
       mbar_init(stage_bar(1), 1);
       for (int b = 0; b < 2; ++b) {
@@ -600,6 +602,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   const bool bias0 = p.pl.bias_l0 != 0;
   const uint32_t idesc = make_idesc_bf16(256, 128);
   const uint32_t a_done_leader = mapa_shared(a_done, 0), b_done_leader = mapa_shared(b_done, 0);
+  const uint32_t b_done1_leader = mapa_shared(b_done1, 0);
   // B descriptors of layer l, image rows [64 h, 64 h + 64) of this CTA
   const bool sine = EXT && p.act == NB_SINE;
   const uint32_t k0steps = p.pl.k_of[0] / 16u;  // layer-1 K-steps (1; 4 with PE)
@@ -665,11 +668,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
   // end of this warp's part of one half's epilogue (its D columns read, its A
   // columns written): one arrive per warp on the leader's barrier, no CTA-wide
   // barrier (the issuer waits for all 32 warps of the pair)
+  // h: 0 = D_a, 1 = the first 16 of the warp's D_b columns, 2 = the other 16
+  // (D_b is signalled in two parts so the issuer starts the next D_a's
+  // K-steps over the first part's features while the second part is stored)
   auto signal = [&](int h) {
     tmem_wait_st();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive_remote_cta(h ? b_done_leader : a_done_leader);
+    if (lane == 0) mbar_arrive_remote_cta(h == 0 ? a_done_leader : (h == 1 ? b_done_leader : b_done1_leader));
   };
   // the 4 column-group-0 warps finished reading a staging buffer
   auto g0_sync = [&]() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
@@ -710,6 +716,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
         __syncwarp();
         NB_TR2(0, 1 | (ln << 8));
         mbar_wait(b_done, bdph);
+        tc_fence_after();
+        if (ln > 0 && elect_one()) {  // K-steps over the features of D_b's first parts
+          const uint64_t bd = bdesc(ln, 0);
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t kk = (j < 2 ? 4u : 12u) + 2u * (j & 1u);  // features 64.., 96.., 192.., 224.. (+0..15)
+            mma_ts2(tmem, A + kk * 8u, bd + (uint64_t)(kk * 16u), idesc, 1u);
+          }
+        }
+        __syncwarp();
+        mbar_wait(b_done1, bdph);
         bdph ^= 1u;
         NB_TR2(0, 2 | (ln << 8));
         tc_fence_after();
@@ -721,8 +738,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
           } else {
             const uint64_t bd = bdesc(ln, 0), bd1 = bdesc(ln, 1);
 #pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) {
-              const uint32_t kk = j < 4 ? j + 4 : j + 8;  // features 64..127, 192..255
+            for (uint32_t j = 0; j < 4; ++j) {
+              const uint32_t kk = (j < 2 ? 5u : 13u) + 2u * (j & 1u);  // the second parts (+16..31)
               mma_ts2(tmem, A + kk * 8u, bd + (uint64_t)(kk * 16u), idesc, 1u);
             }
             mma_commit2(acc_a);
@@ -754,6 +771,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
       }
       signal(0);
       signal(1);
+      signal(2);
     }
     uint32_t s = 0;  // stage counter (acc barrier parity, A buffer)
     int i_tile = 0;  // local tile index
@@ -793,7 +811,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
 #pragma unroll
               for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
             }
-            if (!last) tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
+            if (!last && h == 1) {  // D_b: store and signal the two 16-feature parts apart
+              tmem_st8(trow + ao + (uint32_t)(f0 / 2), *reinterpret_cast<const uint32_t(*)[8]>(pk));
+              signal(1);
+              tmem_st8(trow + ao + (uint32_t)(f0 / 2) + 8u, *reinterpret_cast<const uint32_t(*)[8]>(pk + 8));
+            } else if (!last) {
+              tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
+            }
             NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
             if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
               uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
@@ -828,7 +852,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
             }
           }
           if (tr_reg > 0) NB_TR2(tr_reg, (5 + h * 4) | (l << 8));
-          signal(h);
+          if (h == 0) {
+            signal(0);
+          } else {
+            if (last) signal(1);  // no split store on the last layer (signalled above otherwise)
+            signal(2);
+          }
           if (tr_reg > 0) NB_TR2(tr_reg, (6 + h * 4) | (l << 8));
           if (h == 0 && last && has_next && g == 0) {  // staging buffer (i_tile + 1) & 1 consumed
             g0_sync();
