@@ -398,6 +398,16 @@ class Model:
         return None
 
 
+def set_exit_handoff(mode: str) -> None:
+    """Hand-off between the early-exit segments of nb_score (models with exit
+    heads): "images" (the survivors' bf16 activations, default, faster) or
+    "records" (their fp32 records; the later segments recompute the earlier
+    layers: 8x less DRAM traffic).  Process-wide; counts are identical."""
+    if mode not in ("images", "records"):
+        raise ValueError("mode must be 'images' or 'records'")
+    lib().nb_debug_set_exit_records(1 if mode == "records" else 0)
+
+
 def hier_score(nodes, parent, q: torch.Tensor, y: torch.Tensor, allow_nonfinite: bool = False) -> dict:
     """Neural bounding hierarchy (nb_hier_score): counts of the
     predictor "some root-to-leaf path passes every node"."""

@@ -274,6 +274,7 @@ struct TcPlan<128> { static constexpr int NSLOT = 2, WPS = 8, COLS = 512; };
 template <int W, int LC, int H0C, int H1C, int MODE, int D0C, bool BF, bool EXT = false>
 __global__ void __launch_bounds__(TcPlan<W>::NSLOT * TcPlan<W>::WPS * 32, 1)
     k_fwd_tc(const TcParams p) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   const int L = LC ? LC : p.L;
   const int NH = LC ? ((H0C ? 1 : 0) + (H1C ? 1 : 0)) : p.nh;
   const int h0 = LC ? H0C - 1 : (p.nh > 0 ? p.ha0 - 1 : -1);
@@ -743,8 +744,7 @@ inline cudaError_t launch_tc_wm(const nb_model* m, const FwdArgs& a, cudaStream_
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
-  kern<<<grid, NSLOT * WPS * 32, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(NSLOT * WPS * 32), smem, st, MODE == kTrain, p);
 }
 
 // Generic sine / PE kernels (bias folded; forward, calibrate, score).  D0 > 0:

@@ -507,6 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_fwd_tc2(co
 // K = 64 layer-1 operand in the PE layout (4 K-steps).
 template <int LC, int MODE, int D0, bool EXT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(const TcParams2 p) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   constexpr int W = 256, NEPI = 16, CPT = 32;
   const int L = LC ? LC : p.L;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -970,8 +971,7 @@ static cudaError_t launch_tc2p_m(const nb_model* m, const FwdArgs& a, cudaStream
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const int pairs = (int)std::min<int64_t>(p.num_pairs, m->num_sms / 2);
-  k_fwd_tc2p<LC, MODE, D0, EXT><<<2 * pairs, 576, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(k_fwd_tc2p<LC, MODE, D0, EXT>, dim3(2 * pairs), dim3(576), smem, st, MODE == kTrain, p);
 }
 
 // sine / PE pair kernels (forward, calibrate, score; generic layer count)

@@ -10,6 +10,8 @@
 
 #include "../../include/nb.h"
 
+#include <utility>
+
 namespace nb {
 
 constexpr int kMaxLayers = 8;
@@ -260,6 +262,27 @@ __host__ __device__ inline float key2f(uint32_t k) {
   float f;
   memcpy(&f, &b, 4);
   return f;
+}
+
+
+// Launch a training-chain kernel as a programmatic dependent of the previous
+// kernel in the stream (pdl): its launch and CTA rasterisation overlap the
+// predecessor's tail; the kernel itself calls griddep_wait() before touching
+// memory.  (The fused w = 64 step kernel overlaps its prologue too.)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace nb

@@ -646,6 +646,7 @@ __global__ void k_adam(float* __restrict__ th, float* __restrict__ m, float* __r
 // that updates parameter i also writes every packed copy of it.
 __global__ void k_adam_pack(float* __restrict__ th, float* __restrict__ m, float* __restrict__ v,
                             const float* __restrict__ g, int64_t P, AdamArgs h, PackArgs a) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x)
     adam_pack_one(i, g[i], th, m, v, h, a);
@@ -673,8 +674,8 @@ cudaError_t launch_adam_pack(nb_model* m, float lr, cudaStream_t s) {
   PackArgs a;
   adam_setup(m, lr, &h, &a);
   int blocks = (int)std::min<int64_t>((m->P + 255) / 256, 1024);
-  k_adam_pack<<<blocks, 256, 0, s>>>(m->theta, m->adam_m, m->adam_v, m->grad, m->P, h, a);
-  return cudaGetLastError();
+  return launch_pdl(k_adam_pack, dim3(blocks), dim3(256), 0, s, true, m->theta, m->adam_m, m->adam_v,
+                    (const float*)m->grad, m->P, h, a);
 }
 
 cudaError_t launch_adam(nb_model* m, float lr, cudaStream_t s) {

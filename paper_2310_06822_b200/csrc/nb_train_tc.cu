@@ -51,6 +51,7 @@ __device__ __forceinline__ uint32_t img_off(int r, int fg) {
 // thread owns one row and walks its W columns in 32-column chunks.
 template <int W, bool BITS>
 __global__ void __launch_bounds__(2 * 4 * 32, 1) k_bwd_tc(const BwdParams p) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   constexpr int NSLOT = 2, WPS = 4;
   constexpr int COLS = (NSLOT * (W + W / 2) <= 256) ? 256 : 512;
   static_assert(NSLOT * (W + W / 2) <= 512, "TMEM plan");
@@ -282,6 +283,7 @@ struct DwJobs {
 constexpr int kDwMaxStages = 6;
 
 __global__ void __launch_bounds__(128, 1) k_dw_tc(const __grid_constant__ DwJobs js, int64_t num_tiles) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   const DwJob& j = js.job[blockIdx.y];
   extern __shared__ __align__(1024) uint8_t smem[];
   // stage: A tile 128 features (16 groups) x 128 rows = 32 KB, then B + ones: (fb + 16) x 256 B
@@ -578,8 +580,7 @@ static cudaError_t launch_bwd(nb_model* m, const BwdParams& p, cudaStream_t st) 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(p.num_tiles, m->num_sms);
-  kern<<<grid, 2 * 4 * 32, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(2 * 4 * 32), smem, st, true, p);
 }
 
 static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
@@ -593,8 +594,7 @@ static cudaError_t run_dw(DwJobs& js, int64_t T, cudaStream_t st) {
   const size_t smem = (size_t)js.nst * js.stage + fixed;
   cudaError_t e = cudaFuncSetAttribute(k_dw_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_dw_tc<<<dim3(js.cpj, js.njobs), 128, smem, st>>>(js, T);
-  return cudaGetLastError();
+  return launch_pdl(k_dw_tc, dim3(js.cpj, js.njobs), dim3(128), smem, st, true, js, T);
 }
 
 // Rows per training micro-batch: bounds the scratch (activation / delta

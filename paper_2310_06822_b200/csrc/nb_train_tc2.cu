@@ -37,6 +37,7 @@ __device__ __forceinline__ uint32_t img_off2(int r, int fg) {
 // 16 warps per CTA: warp w reads TMEM lane quarter w % 4 and column group
 // w / 4 (64 of the 256 features of its 32 rows).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_bwd_tc2(const BwdParams2 p) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   constexpr int W = 256, CPT = 64;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -199,6 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) k_bwd_tc2(co
 // k_bwd_tc2's (R34): same bf16 roundings, fp32 accumulation in the MMA.
 template <bool BITS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(544, 1) k_bwd_tc2p(const BwdParams2 p) {
+  griddep_wait();  // programmatic dependent in the training chain (no-op otherwise)
   constexpr int W = 256, NEPI = 16, CPT = 32;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -422,13 +424,11 @@ cudaError_t launch_bwd_tc2(const nb_model* m, const uint8_t* const* h_img, uint8
     auto kern = p.m_img[0] ? k_bwd_tc2p<true> : k_bwd_tc2p<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<2 * pairs, 544, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(2 * pairs), dim3(544), smem, st, true, p);
   }
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_bwd_tc2<<<2 * pairs, 512, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(k_bwd_tc2, dim3(2 * pairs), dim3(512), smem, st, true, p);
 }
 
 }  // namespace nb
