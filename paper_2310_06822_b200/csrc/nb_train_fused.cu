@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(288, 1) k_train_fused2(const FusedParams p) {
       const int fmax = job == 0 ? 16 : 64;
       if (qw * 32 > fmax) continue;
       float* out = p.partial + ((int64_t)(job * gridDim.x + blockIdx.x) * kDwColsF + f) * 128;
-      if (job == L) {  // head: column 0 -> D row 0
+      if (job == L) {  // head: feature f -> row f of partial column 0 (contiguous, reduce kind 4)
         uint32_t w[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(288, 1) k_train_fused2(const FusedParams p) {
               "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
             : "r"(trow + HEAD));
         tmem_wait_ld();
-        if (f <= fmax) out[0] = any ? __uint_as_float(w[0]) : 0.f;
+        if (f <= fmax) p.partial[((int64_t)(job * gridDim.x + blockIdx.x) * kDwColsF) * 128 + f] = any ? __uint_as_float(w[0]) : 0.f;
         continue;
       }
       uint32_t v[64];
@@ -894,8 +894,9 @@ cudaError_t launch_train_fused(nb_model* m, const float* q, const uint8_t* y, in
   *cpj = grid;
   const size_t smem2 = train_fused2_smem(m);
   if (!fused1_forced() && smem2 <= 227 * 1024) {
-    // two tiles in flight; the dW accumulators are transposed (head gradient in D row 0)
-    *head_row = 0;
+    // two tiles in flight; the dW accumulators are transposed: the head
+    // gradient lands in column 0, rows 0..64 of its partial (reduce kind 4)
+    *head_row = -1;
     auto kern = p.L == 4 ? k_train_fused2<4> : (p.L == 3 ? k_train_fused2<3> : k_train_fused2<2>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (e != cudaSuccess) return e;

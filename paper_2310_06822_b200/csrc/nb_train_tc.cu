@@ -252,6 +252,8 @@ struct DwJob {
                  // 1: layer 1: W[m][j] <- D[m][j] + D[m][d0 + j], b[m] <- D[m][16]
                  // 2: head row `row`: v[j] <- D[row][j], c <- D[row][fb]
                  // 3: layer 1 of a PE net (PackLayout::pe_lo): W[m][j] <- D[m][j] + D[m][32 + j], b[m] <- D[m][fb]
+                 // 4: head, transposed partial (k_train_fused2): v[j] <- D[0][row j], c <- D[0][row in]
+                 //    (contiguous per CTA, so the reduce's loads coalesce)
   int rows, row, d0, in;
   float* w_out;
   float* b_out;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
   int jj = 0;
   for (; jj < js.njobs; ++jj) {
     const DwJob& r = js.job[jj];
-    const int total = (r.kind == 2 ? 1 : r.rows) * (r.in + 1);
+    const int total = (r.kind >= 2 && r.kind != 3 ? 1 : r.rows) * (r.in + 1);
     if (e < total) break;
     e -= total;
   }
@@ -463,10 +465,11 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
   int k = 0, m = 0;
   if (active) {
     const DwJob& r = js.job[jj];
-    const unsigned rows = r.kind == 2 ? 1u : (unsigned)r.rows;
+    const bool head = r.kind == 2 || r.kind == 4;
+    const unsigned rows = head ? 1u : (unsigned)r.rows;
     k = (int)((unsigned)e / rows);                        // output column (k == in: bias)
-    m = r.kind == 2 ? r.row : (int)((unsigned)e % rows);  // row of D
-    const int c0 = k == r.in ? r.fb : k;
+    m = r.kind == 2 ? r.row : (r.kind == 4 ? k : (int)((unsigned)e % rows));  // row of D
+    const int c0 = r.kind == 4 ? 0 : (k == r.in ? r.fb : k);
     const int c1 = (k != r.in && r.kind == 1) ? r.d0 + k : ((k != r.in && r.kind == 3) ? 32 + k : -1);
     const float* P = js.partial + ((int64_t)(jj * js.cpj) * kDwCols) * 128 + m;
     const int64_t cs = (int64_t)kDwCols * 128;  // CTA stride
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(32 * kRedSlices) k_dw_reduce(const __grid_cons
     for (int q = 0; q < S; ++q) t += part[q][e_in];
     const DwJob& r = js.job[jj];
     float* out;
-    if (r.kind == 2) {
+    if (r.kind == 2 || r.kind == 4) {
       out = k == r.in ? r.b_out : r.w_out + k;
     } else {
       const int mo = m + r.m_off;
@@ -512,7 +515,7 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
   int64_t total = 0;
   for (int jj = 0; jj < js.njobs; ++jj) {
     const DwJob& r = js.job[jj];
-    total += (int64_t)(r.kind == 2 ? 1 : r.rows) * (r.in + 1);
+    total += (int64_t)(r.kind == 2 || r.kind == 4 ? 1 : r.rows) * (r.in + 1);
   }
   // slices of <= 8 CTA partials each (one round of loads), at most kRedSlices
   const int S = std::max(1, std::min(kRedSlices, (js.cpj + 7) / 8));
@@ -712,6 +715,10 @@ cudaError_t launch_train_tc(nb_model* m, const float* q, const uint8_t* y, int64
     hj = DwJob{nullptr, W, 0, nullptr, W, 2, 1, 64, d0, W, g + m->po.wout, g + m->po.bout};
     cudaError_t e = launch_train_fused(m, q, y, n, n_global, alpha, beta, fj.partial, &fj.cpj, &hj.row, st);
     if (e != cudaSuccess) return e;
+    if (hj.row < 0) {  // k_train_fused2: the head's partial is stored transposed (one contiguous column)
+      hj.kind = 4;
+      hj.row = 0;
+    }
     return launch_dw_reduce(fj, st);
   }
   // dW jobs (image pointers are the same for every micro-batch)
