@@ -518,7 +518,11 @@ static cudaError_t launch_dw_reduce(const DwJobs& js, cudaStream_t st) {
     total += (int64_t)(r.kind == 2 || r.kind == 4 ? 1 : r.rows) * (r.in + 1);
   }
   // slices of <= 8 CTA partials each (one round of loads), at most kRedSlices
-  const int S = std::max(1, std::min(kRedSlices, (js.cpj + 7) / 8));
+  // slices of the CTA range per output group (measured, NB_RED_SLICES sweep:
+  // 148 partials (fused c2) 4 slices 28.9 us per step vs 16: 29.2, 2: 33.9;
+  // 16 partials (c3) 2 slices 76.0 us vs 8: 81.9, 16: 88.0)
+  int S = js.cpj >= 64 ? 4 : std::max(1, std::min(kRedSlices, (js.cpj + 7) / 8));
+  if (const char* ev = getenv("NB_RED_SLICES")) S = std::max(1, std::min(kRedSlices, atoi(ev)));  // measurement
   // a plain launch: as a programmatic dependent of the fused step kernel its
   // 400 CTAs, scheduled early, slowed that kernel's tail (c2 step 30.5 ->
   // 35.9 us, measured); the next step's kernel is the programmatic one
