@@ -803,8 +803,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
               add2p(t[i + 2], t[i + 3], t[i + 2], t[i + 3], b4.z, b4.w);
             }
           }
+          uint32_t pk[16];
           if (!last || MODE == kTrain) {
-            uint32_t pk[16];
             if (sine) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) pk[j] = pack_bf16x2(sin_act(t[2 * j]), sin_act(t[2 * j + 1]));
@@ -812,27 +812,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
 #pragma unroll
               for (int j = 0; j < 16; ++j) pk[j] = pack_relu_bf16x2(t[2 * j], t[2 * j + 1]);
             }
-            if (!last && h == 1) {  // D_b: store and signal the two 16-feature parts apart
+          }
+          if (tr_reg > 0) NB_TR2(tr_reg, (5 + h * 4) | (l << 8));
+          // 1) the accumulator columns are read: hand the issuer the next
+          //    MMAs' operands first (D_b in two 16-feature parts, so the next
+          //    D_a's K-steps over the first part start while the second is stored)
+          if (!last) {
+            if (h == 1) {
               tmem_st8(trow + ao + (uint32_t)(f0 / 2), *reinterpret_cast<const uint32_t(*)[8]>(pk));
               signal(1);
               tmem_st8(trow + ao + (uint32_t)(f0 / 2) + 8u, *reinterpret_cast<const uint32_t(*)[8]>(pk + 8));
-            } else if (!last) {
+              signal(2);
+            } else {
               tmem_st16(trow + ao + (uint32_t)(f0 / 2), pk);
+              signal(0);
             }
-            NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
-            if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
-              uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
+          } else if (h == 0) {
+            if (g == 0 && has_next) encode(next, i_tile + 1, (s + 1) & 1u);  // the next tile's layer-1 operand
+            signal(0);
+          } else {
+            signal(1);
+            signal(2);
+          }
+          if (tr_reg > 0) NB_TR2(tr_reg, (6 + h * 4) | (l << 8));
+          // 2) off the MMA critical path: the training images, the output head
+          NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
+          if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
+            uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4)
-                *reinterpret_cast<uint4*>(base + ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
-                    make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
-              if (p.a.tr.c_img[l]) {  // ReLU'(h) bit mask of my 32 features for the backward (R25, R34)
-                uint32_t mw = 0;
+            for (int q4 = 0; q4 < 4; ++q4)
+              *reinterpret_cast<uint4*>(base + ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+                  make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            if (p.a.tr.c_img[l]) {  // ReLU'(h) bit mask of my 32 features for the backward (R25, R34)
+              uint32_t mw = 0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  mw |= ((pk[j] & 0x7FFFu) ? 1u : 0u) << (2 * j) | ((pk[j] & 0x7FFF0000u) ? 1u : 0u) << (2 * j + 1);
-                reinterpret_cast<uint32_t*>(p.a.tr.c_img[l] + (2 * tile + rank) * 4096)[(f0 / 32) * 128 + rit] = mw;
-              }
+              for (int j = 0; j < 16; ++j)
+                mw |= ((pk[j] & 0x7FFFu) ? 1u : 0u) << (2 * j) | ((pk[j] & 0x7FFF0000u) ? 1u : 0u) << (2 * j + 1);
+              reinterpret_cast<uint32_t*>(p.a.tr.c_img[l] + (2 * tile + rank) * 4096)[(f0 / 32) * 128 + rit] = mw;
             }
           }
           if (last) {
@@ -845,21 +861,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
               for (int i = 0; i < CPT; i += 2)
                 fma2p(zp, zq, relu_nan(t[i]), relu_nan(t[i + 1]), wo[i], wo[i + 1]);
             }
-            if (h == 0 && g == 0 && has_next) encode(next, i_tile + 1, (s + 1) & 1u);
             if (h == 1) {  // this group's partial of the output logit -> the classifier
               xch[((i_tile & 1) * 4 + g) * 128 + rit] = zp + zq;
               __syncwarp();
               if (lane == 0) mbar_arrive(xfull(i_tile & 1));
             }
           }
-          if (tr_reg > 0) NB_TR2(tr_reg, (5 + h * 4) | (l << 8));
-          if (h == 0) {
-            signal(0);
-          } else {
-            if (last) signal(1);  // no split store on the last layer (signalled above otherwise)
-            signal(2);
-          }
-          if (tr_reg > 0) NB_TR2(tr_reg, (6 + h * 4) | (l << 8));
           if (h == 0 && last && has_next && g == 0) {  // staging buffer (i_tile + 1) & 1 consumed
             g0_sync();
             stage_issue(next + 2 * npairs, (i_tile + 1) & 1);
