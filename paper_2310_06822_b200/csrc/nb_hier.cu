@@ -8,7 +8,8 @@
 // included).  Evaluation prunes like a BVH: a node runs only on the rows its
 // parent passed — the rows are gathered into a dense array, scored by the
 // node's fused forward kernel, and the passing rows compacted into the
-// node's survivor list; leaves mark their survivors.  The compaction is
+// node's survivor list; leaves mark their survivors (consecutive siblings
+// share their parent's gather).  The compaction is
 // order-preserving (two passes over fixed row chunks: survivor counts, then
 // each chunk writes at the prefix of the counts before it), so every
 // survivor list is ascending and the next node's gather reads the records in
@@ -217,6 +218,7 @@ cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* paren
   if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (5 + n_nodes), st);
   std::vector<char> is_leaf(n_nodes, 1);
   for (int i = 1; i < n_nodes; ++i) is_leaf[parent[i]] = 0;
+  int gathered = -1;  // the node whose survivors qg holds (siblings share one gather)
   for (int i = 0; i < n_nodes && e == cudaSuccess && n > 0; ++i) {
     const nb_model* m = nodes[i];
     const int nl = 1 + m->d.n_heads;
@@ -228,7 +230,8 @@ cudaError_t hier_score(nb_model* const* nodes, int n_nodes, const int32_t* paren
     } else {
       const int32_t* in = idx + (size_t)parent[i] * (idx_bytes / 4);
       const unsigned long long* c_in = node_cnt + parent[i];
-      k_gather<<<grid_for(n), 256, 0, st>>>(q, in, c_in, d0, qg);
+      if (gathered != parent[i]) k_gather<<<grid_for(n), 256, 0, st>>>(q, in, c_in, d0, qg);
+      gathered = parent[i];
       e = forward(m, qg, n, c_in, lg, st);
       if (e != cudaSuccess) break;
       compact(m, in, 0, c_in, out, node_cnt + i);

@@ -165,3 +165,40 @@ def test_gpu_hierarchy_nonfinite_and_scratch_reuse():
     c = nb.hier_score(models, [-1, 0, 0], bad.cuda(), yd, allow_nonfinite=True)
     assert c["nonfinite"] == len(rows)
     assert c["tp"] + c["fp"] == n - len(rows) and c["tp"] + c["fp"] + c["fn"] + c["tn"] == n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parent", [[-1, 0, 1, 1, 0, 4, 4], [-1, 0, 0, 1, 2, 1, 2]])
+def test_gpu_hierarchy_depth2_interleaved_siblings(parent):
+    """Seven fp32 nodes, depth 2, in depth-first order (siblings 2/3 and 5/6
+    consecutive, 1 and 4 not) and in an order where no two consecutive nodes
+    share a parent: every node's gather (shared by consecutive siblings) must
+    see its own parent's survivors.  Counts equal the oracle's combination
+    exactly away from the thresholds."""
+    import paper_2310_06822_b200 as nb
+    from gpu_helpers import grid_of
+    cfg = nbgen.CONFIGS["c1"]
+    n = 3 * 4096 + 11
+    q = nbgen.make_queries(cfg, nbgen.TAG_EVAL, 1, n)
+    y = oracle.label(grid_of(cfg), 2, "point", q.numpy())
+    qd, yd = q.cuda(), torch.from_numpy(y).cuda()
+    a = oracle.make_arch(2, 32, 2)
+    models, thetas, taus = [], [], []
+    for i in range(len(parent)):
+        th = torch.from_numpy(np.random.default_rng(40 + i).normal(size=oracle.num_params(a)) * 0.6).float()
+        m = nb.Model(nb.Desc("point", 2, 32, 2, (), "fp32"), 0)
+        m.set_params(th)
+        t = float(np.quantile(oracle.forward(a, th.double().numpy(), q.numpy()[:2000])[:, 0], 0.3))
+        m.set_thresholds([t])
+        models.append(m)
+        thetas.append(th.double().numpy())
+        taus.append(t)
+    z = [oracle.forward(a, th, q.numpy())[:, 0] for th in thetas]
+    keep = np.all([np.abs(zi - t) > 1e-4 for zi, t in zip(z, taus)], axis=0)
+    pred = oracle.hier_combine(parent, [zi >= np.float32(t) for zi, t in zip(z, taus)])
+    c = nb.hier_score(models, parent, qd[torch.from_numpy(keep).cuda()], yd[torch.from_numpy(keep).cuda()])
+    yy = y[keep].astype(bool)
+    p = pred[keep]
+    assert 0.05 < p.mean() < 0.95  # pruning happens at every level
+    assert (c["tp"], c["fp"], c["fn"], c["tn"]) == (int((p & yy).sum()), int((p & ~yy).sum()),
+                                                    int((~p & yy).sum()), int((~p & ~yy).sum()))
