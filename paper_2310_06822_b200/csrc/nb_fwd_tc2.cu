@@ -838,10 +838,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1) k_fwd_tc2p(c
           // 2) off the MMA critical path: the training images, the output head
           NB_CHECK(f0 % 32 == 0 && f0 + CPT <= W);
           if (MODE == kTrain && 2 * tile + rank < p.a.tr.num_tiles) {  // h_{l+1} image (R34 masks, dW)
-            uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W);
+            // core-matrix offset ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16 written as
+            // f0 * 256 + (row part) + q4 * 2048 (f0 % 32 == 0): one base register, immediate
+            // offsets per store (the per-(half, q4) offsets the compiler hoisted were spilled)
+            uint8_t* base = p.a.tr.h_img[l] + (2 * tile + rank) * img_tile_bytes(W) +
+                            ((uint32_t)f0 * 256u + (uint32_t)(rit / 8) * 128u + (uint32_t)(rit % 8) * 16u);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<uint4*>(base + ((f0 / 8 + q4) * 16 + rit / 8) * 128 + (rit % 8) * 16) =
+              *reinterpret_cast<uint4*>(base + q4 * 2048) =
                   make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
             if (p.a.tr.c_img[l]) {  // ReLU'(h) bit mask of my 32 features for the backward (R25, R34)
               uint32_t mw = 0;
